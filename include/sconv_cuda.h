@@ -1,0 +1,213 @@
+/*
+ * sconv_cuda.h -- C ABI of the B200 (sm_100a) ECR / PECR sparse-convolution
+ * library (libsconv_cuda.so).
+ *
+ * This is the thin layer the reference's C++ host API calls into.  Plain
+ * pointers and sizes only; no C++ or torch types cross it.  Each entry point
+ * names the reference interface it replaces (paths relative to
+ * /root/reference/proj).  Layouts follow FeatureMap/Filter
+ * (include/sconv/tensor.hpp:12-49): channel-major then row-major fp32.
+ *
+ *   x  [N][C][H][W]   input maps (valid convolution, no padding)
+ *   w  [K][C][kh][kw] filters (one Filter per output channel, as in
+ *                     LayerSpec::filters, include/sconv/pipeline.hpp:17-23)
+ *   y  [N][K][oh][ow] ECR output, or [N][K][packs_h][packs_w] PECR output
+ *
+ * Error model: every function returns an sconv_status.  The C++ drop-in
+ * (paper_1909_09927_b200/csrc/dropin/) maps them onto the reference
+ * exception types of include/sconv/errors.hpp:9-26 and exec.hpp:43-51.
+ * sconv_cu_last_error() holds the message of the last failure on a context.
+ *
+ * Threading: a context owns one CUDA stream on one device and is not safe to
+ * share between host threads without external synchronisation; any number of
+ * contexts may run concurrently (the reference's "pure and reentrant"
+ * contract).
+ */
+#ifndef SCONV_CUDA_H
+#define SCONV_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCONV_CUDA_ABI_VERSION 1
+
+typedef enum {
+  SCONV_OK = 0,
+  SCONV_ERR_SHAPE = 1,    /* sconv::ShapeError   (errors.hpp:9-12)  */
+  SCONV_ERR_CONFIG = 2,   /* sconv::ConfigError  (errors.hpp:14-17) */
+  SCONV_ERR_FORMAT = 3,   /* sconv::FormatError  (errors.hpp:19-22) */
+  SCONV_ERR_IO = 4,       /* sconv::IoError      (errors.hpp:24-26) */
+  SCONV_ERR_DISPATCH = 5, /* sconv::DispatchError (exec.hpp:43-51)  */
+  SCONV_ERR_CUDA = 6,     /* device / runtime failure -> std::runtime_error */
+  SCONV_ERR_ARG = 7       /* null pointer or bad handle -> std::invalid_argument */
+} sconv_status;
+
+/* ---- flags ------------------------------------------------------------ */
+/* Arithmetic.  EXACT (default) accumulates every output in the reference's
+ * c -> i -> j order with separately rounded multiply and add: bit-identical
+ * to ecr_spmv_conv / pecr_conv_pool.  FAST contracts each term into one FFMA
+ * (same order); results stay within |a-b| <= 1e-5 + 1e-5*|b| of the
+ * reference. */
+#define SCONV_F_EXACT 0u
+#define SCONV_F_FAST (1u << 0)
+/* Every tensor pointer is a device pointer on the context's device (no
+ * host<->device copies).  Without it all pointers are host pointers. */
+#define SCONV_F_DEVICE (1u << 1)
+/* With SCONV_F_DEVICE: return right after enqueueing on the context stream
+ * (no stream synchronisation).  Counters must then be NULL. */
+#define SCONV_F_ASYNC (1u << 2)
+/* Force the generic (one thread per output) kernels; testing only. */
+#define SCONV_F_GENERIC (1u << 3)
+
+typedef enum { SCONV_POOL_MAX = 0, SCONV_POOL_MEAN = 1 } sconv_pool_mode;
+
+typedef struct sconv_cu_ctx sconv_cu_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+const char* sconv_cu_version(void);
+int sconv_cu_device_count(int* count);
+int sconv_cu_ctx_create(int device, sconv_cu_ctx** out);
+int sconv_cu_ctx_destroy(sconv_cu_ctx* ctx);
+/* Run on an external cudaStream_t (e.g. torch's current stream); NULL
+ * restores the context's own stream. */
+int sconv_cu_ctx_set_stream(sconv_cu_ctx* ctx, void* stream);
+void* sconv_cu_ctx_stream(sconv_cu_ctx* ctx);
+int sconv_cu_ctx_device(sconv_cu_ctx* ctx);
+int sconv_cu_synchronize(sconv_cu_ctx* ctx);
+const char* sconv_cu_last_error(const sconv_cu_ctx* ctx);
+/* Number of kernels this context has launched (evidence counter). */
+uint64_t sconv_cu_launch_count(const sconv_cu_ctx* ctx);
+
+/* ---- geometry (host only) ---------------------------------------------- */
+/* conv_output_dims, src/tensor.cpp:44-55. */
+int sconv_conv_output_dims(int in_w, int in_h, int k_w, int k_h, int stride,
+                           int* out_w, int* out_h);
+/* pecr_pack_count (Eq. 3), src/pecr.cpp:62-81. */
+int sconv_pecr_pack_count(int in_extent, int k_extent, int conv_stride,
+                          int pool_extent, int pool_stride, int* packs);
+
+/* The CUDA launch chosen for a layer (replaces the simulated grid of
+ * plan(), src/exec.cpp:8-36, for reporting).  pool_w == 0 -> ECR. */
+typedef struct {
+  int kernel;          /* 0 generic, 1 tiled 3x3, ... */
+  int grid_x, grid_y, grid_z;
+  int block_threads;
+  int smem_bytes;
+  int tile_h, tile_w, tile_k; /* outputs per CTA */
+} sconv_launch_plan;
+int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
+                  int pool_w, int pool_h, int pool_stride, unsigned flags,
+                  sconv_launch_plan* out);
+
+/* ---- hot path: fused, batched ------------------------------------------ */
+/* ECR convolution of N maps by K filters.  Replaces the per-filter
+ * ecr_convert -> ecr_spmv_conv pair (src/ecr.cpp:51-128) as driven by
+ * multichannel_conv (src/pipeline.cpp:191-210): the window compaction is done
+ * on chip and never written to HBM.  Windows with no nonzero produce +0.0
+ * (ptr == -1 law, ecr.cpp:112-115).  muls/adds (optional, accumulated with
+ * +=) equal the sum over all (image, filter) calls of OpCount from
+ * ecr_spmv_conv: per window nnz and max(nnz-1, 0). */
+int sconv_cu_ecr_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h,
+                      int w, const float* filters, int k, int kh, int kw,
+                      int stride, float* y, uint64_t* muls, uint64_t* adds,
+                      unsigned flags);
+
+/* PECR fused convolution + ReLU + pooling.  Replaces pecr_convert ->
+ * pecr_conv_pool (src/pecr.cpp:83-172) as driven by forward's fused branch
+ * (src/pipeline.cpp:249-264).  Max mode starts the running max at +0.0
+ * (ReLU folded, pecr.cpp:149,157-158); mean mode sums max(acc, 0) over the
+ * p_w*p_h windows in raster order then divides (pecr.cpp:159-167).  The
+ * pre-pool convolution output never reaches HBM.  ConfigError unless Eq. 3
+ * tiles both axes exactly. */
+int sconv_cu_pecr_conv_pool(sconv_cu_ctx* ctx, const float* x, int n, int c,
+                            int h, int w, const float* filters, int k, int kh,
+                            int kw, int stride, int pool_w, int pool_h,
+                            int pool_stride, int mode, float* y,
+                            uint64_t* muls, uint64_t* adds, unsigned flags);
+
+/* ---- formats: the reference's two-phase API (one map, one filter) ------- */
+/* ecr_convert (src/ecr.cpp:51-97) by warp-ballot compaction.  Writes the
+ * fixed-slot EcrMap arrays of include/sconv/ecr.hpp:35-45, flattened
+ * [oh][ow][slot] (slot = c*kh*kw): nonzeros in c->i->j order, their paired
+ * weights and offsets, filler 0.0 / 0.0 / -1, and ptr[oh][ow] = nnz or -1. */
+int sconv_cu_ecr_convert(sconv_cu_ctx* ctx, const float* x, int c, int h,
+                         int w, const float* filter, int kh, int kw, int stride,
+                         int32_t* ptr, int32_t* offsets, float* f_data,
+                         float* k_data, unsigned flags);
+
+/* ecr_spmv_conv (src/ecr.cpp:99-128) over an EcrMap: FormatError when a ptr
+ * lies outside [-1, slot] (check_ecr, ecr.cpp:22-42). */
+int sconv_cu_ecr_spmv(sconv_cu_ctx* ctx, const int32_t* ptr,
+                      const float* f_data, const float* k_data, int oh, int ow,
+                      int slot, float* y, uint64_t* muls, uint64_t* adds,
+                      unsigned flags);
+
+/* pecr_convert (src/pecr.cpp:83-131), phase 1: per pack and window nonzero
+ * counts count[packs_h][packs_w][pool_w*pool_h] and the exclusive prefix
+ * pack_start[packs_h*packs_w + 1]; *total = entries of the whole map. */
+int sconv_cu_pecr_count(sconv_cu_ctx* ctx, const float* x, int c, int h, int w,
+                        int kh, int kw, int stride, int pool_w, int pool_h,
+                        int pool_stride, int32_t* count, int64_t* pack_start,
+                        int64_t* total, unsigned flags);
+/* phase 2: data/index of every pack, concatenated pack-major
+ * (PecrPoolPack::data / index, include/sconv/pecr.hpp:39-43). */
+int sconv_cu_pecr_fill(sconv_cu_ctx* ctx, const float* x, int c, int h, int w,
+                       int kh, int kw, int stride, int pool_w, int pool_h,
+                       int pool_stride, const int64_t* pack_start, int64_t total,
+                       float* data, int32_t* index, unsigned flags);
+
+/* pecr_conv_pool (src/pecr.cpp:133-172) over a PecrMap; FormatError on the
+ * check_pecr violations of pecr.cpp:24-58 (count range, data/index length,
+ * index range). */
+int sconv_cu_pecr_pool(sconv_cu_ctx* ctx, const int32_t* count,
+                       const int64_t* pack_start, const float* data,
+                       const int32_t* index, int64_t total,
+                       const float* kernel, int c, int kh, int kw, int packs_h,
+                       int packs_w, int pool_w, int pool_h, int mode, float* y,
+                       uint64_t* muls, uint64_t* adds, unsigned flags);
+
+/* ---- multi-GPU partition (replaces dispatch's worker partition,
+ *      include/sconv/exec.hpp:89-107) --------------------------------------
+ * Contiguous shard of the (image, filter) grid owned by `rank` of `world`:
+ * images are split when n >= world, otherwise output channels.  Every output
+ * is produced by exactly one rank with the same per-output order, so results
+ * are bit-identical for any world size. */
+int sconv_shard(int n, int k, int world, int rank, int* n_begin, int* n_end,
+                int* k_begin, int* k_end);
+
+/* One host thread driving several devices (dispatch's fork/join over GPUs):
+ * shards by sconv_shard, runs every context's stream concurrently, joins.
+ * Host pointers only. */
+int sconv_cu_ecr_conv_multi(sconv_cu_ctx** ctxs, int nctx, const float* x,
+                            int n, int c, int h, int w, const float* filters,
+                            int k, int kh, int kw, int stride, float* y,
+                            uint64_t* muls, uint64_t* adds, unsigned flags);
+int sconv_cu_pecr_conv_pool_multi(sconv_cu_ctx** ctxs, int nctx,
+                                  const float* x, int n, int c, int h, int w,
+                                  const float* filters, int k, int kh, int kw,
+                                  int stride, int pool_w, int pool_h,
+                                  int pool_stride, int mode, float* y,
+                                  uint64_t* muls, uint64_t* adds,
+                                  unsigned flags);
+
+/* ---- synthetic inputs (host) ------------------------------------------- */
+/* Bit-identical to sconv::generate (src/dataset.cpp:77-100): xoshiro256**
+ * seeded by SplitMix64, floor(s*N) zeros at Fisher-Yates positions, nonzeros
+ * in (0,1].  The batch form fills maps[i] = generate(h, w, c, s, seeds[i])
+ * with up to `threads` host threads (0 = all cores). */
+int sconv_generate(int height, int width, int channels, double sparsity,
+                   uint64_t seed, float* out);
+int sconv_generate_batch(int count, int height, int width, int channels,
+                         double sparsity, const uint64_t* seeds, float* out,
+                         int threads);
+/* checksum_hex (src/report.cpp:14-30) as an integer: FNV-1a 64. */
+uint64_t sconv_checksum(const float* values, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCONV_CUDA_H */

@@ -1,0 +1,145 @@
+"""ctypes binding of libsconv_cuda.so (include/sconv_cuda.h).
+
+The library is built in-tree by ``paper_1909_09927_b200/csrc/Makefile``
+(``__graft_entry__.build()``).  There is no fallback: if the shared object is
+missing, importing the compute API raises ImportError, and on a machine
+without a B200 every device entry point fails with CudaError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import raise_for
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libsconv_cuda.so")
+
+# exported symbols (kept in sync with include/sconv_cuda.h; tests check both)
+SYMBOLS = (
+    "sconv_cu_version", "sconv_cu_device_count", "sconv_cu_ctx_create", "sconv_cu_ctx_destroy",
+    "sconv_cu_ctx_set_stream", "sconv_cu_ctx_stream", "sconv_cu_ctx_device",
+    "sconv_cu_synchronize", "sconv_cu_last_error", "sconv_cu_launch_count",
+    "sconv_conv_output_dims", "sconv_pecr_pack_count", "sconv_cu_plan", "sconv_cu_ecr_conv",
+    "sconv_cu_pecr_conv_pool", "sconv_cu_ecr_convert", "sconv_cu_ecr_spmv", "sconv_cu_pecr_count",
+    "sconv_cu_pecr_fill", "sconv_cu_pecr_pool", "sconv_shard", "sconv_cu_ecr_conv_multi",
+    "sconv_cu_pecr_conv_pool_multi", "sconv_generate", "sconv_generate_batch", "sconv_checksum",
+)
+
+F_EXACT = 0
+F_FAST = 1 << 0
+F_DEVICE = 1 << 1
+F_ASYNC = 1 << 2
+F_GENERIC = 1 << 3
+
+_vp = C.c_void_p
+_i = C.c_int
+_u64p = C.POINTER(C.c_uint64)
+
+
+class LaunchPlan(C.Structure):
+    _fields_ = [("kernel", _i), ("grid_x", _i), ("grid_y", _i), ("grid_z", _i),
+                ("block_threads", _i), ("smem_bytes", _i), ("tile_h", _i), ("tile_w", _i),
+                ("tile_k", _i)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libsconv_cuda.so once; raise ImportError when it was never built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libsconv_cuda.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    L.sconv_cu_version.restype = C.c_char_p
+    L.sconv_cu_device_count.argtypes = [C.POINTER(_i)]
+    L.sconv_cu_ctx_create.argtypes = [_i, C.POINTER(_vp)]
+    L.sconv_cu_ctx_destroy.argtypes = [_vp]
+    L.sconv_cu_ctx_set_stream.argtypes = [_vp, _vp]
+    L.sconv_cu_ctx_stream.argtypes = [_vp]
+    L.sconv_cu_ctx_stream.restype = _vp
+    L.sconv_cu_ctx_device.argtypes = [_vp]
+    L.sconv_cu_synchronize.argtypes = [_vp]
+    L.sconv_cu_last_error.argtypes = [_vp]
+    L.sconv_cu_last_error.restype = C.c_char_p
+    L.sconv_cu_launch_count.argtypes = [_vp]
+    L.sconv_cu_launch_count.restype = C.c_uint64
+    L.sconv_conv_output_dims.argtypes = [_i] * 5 + [C.POINTER(_i)] * 2
+    L.sconv_pecr_pack_count.argtypes = [_i] * 5 + [C.POINTER(_i)]
+    L.sconv_cu_plan.argtypes = [_i] * 11 + [C.c_uint, C.POINTER(LaunchPlan)]
+    L.sconv_cu_ecr_conv.argtypes = [_vp, _vp] + [_i] * 4 + [_vp] + [_i] * 4 + [_vp, _u64p, _u64p,
+                                                                               C.c_uint]
+    L.sconv_cu_pecr_conv_pool.argtypes = [_vp, _vp] + [_i] * 4 + [_vp] + [_i] * 8 + [
+        _vp, _u64p, _u64p, C.c_uint]
+    L.sconv_cu_ecr_convert.argtypes = [_vp, _vp] + [_i] * 3 + [_vp] + [_i] * 3 + [_vp] * 4 + [
+        C.c_uint]
+    L.sconv_cu_ecr_spmv.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 3 + [_vp, _u64p, _u64p, C.c_uint]
+    L.sconv_cu_pecr_count.argtypes = [_vp, _vp] + [_i] * 9 + [_vp, _vp, C.POINTER(C.c_int64),
+                                                             C.c_uint]
+    L.sconv_cu_pecr_fill.argtypes = [_vp, _vp] + [_i] * 9 + [_vp, C.c_int64, _vp, _vp, C.c_uint]
+    L.sconv_cu_pecr_pool.argtypes = [_vp, _vp, _vp, _vp, _vp, C.c_int64, _vp] + [_i] * 8 + [
+        _vp, _u64p, _u64p, C.c_uint]
+    L.sconv_shard.argtypes = [_i] * 4 + [C.POINTER(_i)] * 4
+    L.sconv_cu_ecr_conv_multi.argtypes = [C.POINTER(_vp), _i, _vp] + [_i] * 4 + [_vp] + [
+        _i] * 4 + [_vp, _u64p, _u64p, C.c_uint]
+    L.sconv_cu_pecr_conv_pool_multi.argtypes = [C.POINTER(_vp), _i, _vp] + [_i] * 4 + [_vp] + [
+        _i] * 8 + [_vp, _u64p, _u64p, C.c_uint]
+    L.sconv_generate.argtypes = [_i, _i, _i, C.c_double, C.c_uint64, _vp]
+    L.sconv_generate_batch.argtypes = [_i, _i, _i, _i, C.c_double, _vp, _vp, _i]
+    L.sconv_checksum.argtypes = [_vp, C.c_int64]
+    L.sconv_checksum.restype = C.c_uint64
+    _lib = L
+    return L
+
+
+def check(status: int, ctx=None) -> None:
+    if status:
+        msg = lib().sconv_cu_last_error(ctx)
+        raise_for(status, msg.decode() if msg else f"status {status}")
+
+
+class Context:
+    """One device + one stream + workspace (sconv_cu_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = _vp()
+        check(lib().sconv_cu_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+        self._stream = None
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        if stream_ptr != self._stream:
+            check(lib().sconv_cu_ctx_set_stream(self.handle, stream_ptr), self.handle)
+            self._stream = stream_ptr
+
+    def synchronize(self) -> None:
+        check(lib().sconv_cu_synchronize(self.handle), self.handle)
+
+    @property
+    def launches(self) -> int:
+        return int(lib().sconv_cu_launch_count(self.handle))
+
+    def close(self) -> None:
+        if self.handle:
+            lib().sconv_cu_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_contexts: dict[int, Context] = {}
+
+
+def context(device: int = 0) -> Context:
+    ctx = _contexts.get(device)
+    if ctx is None:
+        ctx = _contexts[device] = Context(device)
+    return ctx

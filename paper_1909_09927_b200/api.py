@@ -1,0 +1,630 @@
+"""Python mirror of the reference host API for the ECR / PECR hot path.
+
+Names, argument meaning and error behaviour follow the reference's C++ API
+(include/sconv/{tensor,ecr,pecr,exec,metrics,dataset,report}.hpp); every
+compute call goes through libsconv_cuda.so (include/sconv_cuda.h) on a B200.
+There is no CPU fallback.
+
+Two layers:
+
+* the reference's per-(map, filter) two-phase calls -- ``ecr_convert`` /
+  ``ecr_spmv_conv`` / ``pecr_convert`` / ``pecr_conv_pool`` -- which
+  materialise the ECR / PECR formats exactly as the reference lays them out
+  (bit-exact index, count and value arrays), and
+* the batched fused entries -- ``ecr_conv_batched`` and
+  ``pecr_conv_pool_batched`` -- that take N maps x K filters (numpy on the
+  host, or torch CUDA tensors already in HBM) and never write the format.
+
+``ExecConfig.fast`` selects FFMA arithmetic; the default EXACT mode is
+bit-identical to the reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ConfigError, FormatError, ShapeError
+
+# ---------------------------------------------------------------------------
+# value types (include/sconv/tensor.hpp:12-62, metrics.hpp:11-21)
+# ---------------------------------------------------------------------------
+
+
+def _check_dims(c: int, h: int, w: int, what: str) -> None:
+    if c < 1 or h < 1 or w < 1:  # tensor.cpp:11-18
+        raise ShapeError(f"{what} dims must be positive, got {c}x{h}x{w}")
+
+
+@dataclass(eq=False)
+class FeatureMap:
+    """Dense C x H x W fp32 map; (c, y, x) at c*H*W + y*W + x (tensor.hpp:12-30)."""
+    channels: int
+    height: int
+    width: int
+    values: np.ndarray = None
+
+    def __post_init__(self):
+        _check_dims(self.channels, self.height, self.width, "feature map")
+        n = self.channels * self.height * self.width
+        if self.values is None:
+            self.values = np.zeros(n, np.float32)
+        else:
+            self.values = np.ascontiguousarray(self.values, np.float32).reshape(-1)
+            if self.values.size != n:
+                raise ShapeError("feature map value count does not match dims")
+
+    def size(self) -> int:
+        return int(self.values.size)
+
+    def offset(self, c: int, y: int, x: int) -> int:
+        return (c * self.height + y) * self.width + x
+
+    def at(self, c: int, y: int, x: int) -> float:
+        return float(self.values[self.offset(c, y, x)])
+
+    def array(self) -> np.ndarray:
+        return self.values.reshape(self.channels, self.height, self.width)
+
+    def __eq__(self, other):
+        return (isinstance(other, FeatureMap) and
+                (self.channels, self.height, self.width) ==
+                (other.channels, other.height, other.width) and
+                np.array_equal(self.values.view(np.uint32), other.values.view(np.uint32)))
+
+
+@dataclass(eq=False)
+class Filter:
+    """One convolution kernel, same layout as FeatureMap (tensor.hpp:34-49)."""
+    channels: int
+    height: int
+    width: int
+    weights: np.ndarray
+
+    def __post_init__(self):
+        _check_dims(self.channels, self.height, self.width, "filter")
+        self.weights = np.ascontiguousarray(self.weights, np.float32).reshape(-1)
+        if self.weights.size != self.channels * self.height * self.width:
+            raise ShapeError("filter weight count does not match dims")
+
+    def size(self) -> int:
+        return int(self.weights.size)
+
+    def at(self, c: int, i: int, j: int) -> float:
+        return float(self.weights[(c * self.height + i) * self.width + j])
+
+    def array(self) -> np.ndarray:
+        return self.weights.reshape(self.channels, self.height, self.width)
+
+
+@dataclass
+class ConvConfig:
+    stride: int = 1
+
+
+class PoolMode(enum.IntEnum):
+    kMax = 0
+    kMean = 1
+    MAX = 0
+    MEAN = 1
+
+
+@dataclass
+class PoolConfig:
+    width: int = 0
+    height: int = 0
+    stride: int = 1
+    mode: PoolMode = PoolMode.kMax
+
+
+@dataclass
+class ExecConfig:
+    """exec.hpp:30-33 plus the device-side knobs.
+
+    ``workers`` keeps the reference's meaning (host worker threads, must be
+    >= 1) -- results never depend on it; on the GPU the partition is the CUDA
+    grid.  ``device`` picks the B200, ``fast`` selects FFMA arithmetic.
+    """
+    workers: int = 1
+    shared_memory_budget: int = 49152
+    device: int = 0
+    fast: bool = False
+
+
+@dataclass
+class OpCount:
+    multiplications: int = 0
+    additions: int = 0
+
+    def merge(self, other: "OpCount") -> None:
+        self.multiplications += other.multiplications
+        self.additions += other.additions
+
+
+@dataclass
+class OutputDims:
+    width: int = 0
+    height: int = 0
+
+
+# ---------------------------------------------------------------------------
+# ECR format (include/sconv/ecr.hpp:11-45)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class EcrDims:
+    in_w: int = 0
+    in_h: int = 0
+    k_w: int = 0
+    k_h: int = 0
+    stride: int = 1
+    channels: int = 1
+
+    def out_w(self) -> int:
+        return (self.in_w - self.k_w) // self.stride + 1
+
+    def out_h(self) -> int:
+        return (self.in_h - self.k_h) // self.stride + 1
+
+    def slot(self) -> int:
+        return self.channels * self.k_w * self.k_h
+
+
+@dataclass
+class EcrBlockRow:
+    f_data: np.ndarray
+    k_data: np.ndarray
+    offsets: np.ndarray
+    ptr: np.ndarray
+
+
+@dataclass
+class EcrMap:
+    dims: EcrDims
+    block_rows: List[EcrBlockRow] = field(default_factory=list)
+
+
+@dataclass
+class EcrGridShape:
+    blocks: int = 0
+    threads_per_block: int = 0
+
+
+# ---------------------------------------------------------------------------
+# PECR format (include/sconv/pecr.hpp:18-52)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class PecrDims:
+    in_w: int = 0
+    in_h: int = 0
+    k_w: int = 0
+    k_h: int = 0
+    conv_stride: int = 1
+    channels: int = 1
+    pool: PoolConfig = field(default_factory=PoolConfig)
+
+    def tile_w(self) -> int:
+        return self.k_w + self.conv_stride * (self.pool.width - 1)
+
+    def tile_h(self) -> int:
+        return self.k_h + self.conv_stride * (self.pool.height - 1)
+
+    def windows_per_pack(self) -> int:
+        return self.pool.width * self.pool.height
+
+    def capacity(self) -> int:
+        return self.windows_per_pack() * self.channels * self.k_w * self.k_h
+
+
+@dataclass
+class PecrPoolPack:
+    data: np.ndarray
+    index: np.ndarray
+    count: np.ndarray
+
+
+@dataclass
+class PecrMap:
+    dims: PecrDims
+    kernel: np.ndarray
+    pool_rows: List[List[PecrPoolPack]] = field(default_factory=list)
+
+    def packs_w(self) -> int:
+        return len(self.pool_rows[0]) if self.pool_rows else 0
+
+    def packs_h(self) -> int:
+        return len(self.pool_rows)
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _flags(exec_cfg: ExecConfig, extra: int = 0) -> int:
+    if exec_cfg.workers < 1:
+        raise ConfigError("workers must be >= 1")  # exec.hpp:62
+    return (nat.F_FAST if exec_cfg.fast else nat.F_EXACT) | extra
+
+
+def _ctx(exec_cfg: ExecConfig) -> nat.Context:
+    return nat.context(exec_cfg.device)
+
+
+def conv_output_dims(in_w: int, in_h: int, k_w: int, k_h: int, stride: int) -> OutputDims:
+    """tensor.cpp:44-55 (floor semantics, ShapeError / ConfigError)."""
+    ow, oh = C.c_int(), C.c_int()
+    nat.check(nat.lib().sconv_conv_output_dims(in_w, in_h, k_w, k_h, stride, C.byref(ow),
+                                               C.byref(oh)))
+    return OutputDims(ow.value, oh.value)
+
+
+def ecr_grid_shape(in_w: int, in_h: int, k_w: int, k_h: int, stride: int) -> EcrGridShape:
+    """(blocks, threads) = (output rows, output cols), ecr.cpp:46-49."""
+    d = conv_output_dims(in_w, in_h, k_w, k_h, stride)
+    return EcrGridShape(d.height, d.width)
+
+
+def pecr_pack_count(in_extent: int, k_extent: int, conv_stride: int, pool_extent: int,
+                    pool_stride: int) -> int:
+    """Eq. 3 with exact-divisibility check, pecr.cpp:62-81."""
+    out = C.c_int()
+    nat.check(nat.lib().sconv_pecr_pack_count(in_extent, k_extent, conv_stride, pool_extent,
+                                              pool_stride, C.byref(out)))
+    return out.value
+
+
+# ---------------------------------------------------------------------------
+# ECR two-phase API
+# ---------------------------------------------------------------------------
+
+
+def ecr_convert(map: FeatureMap, filter: Filter, cfg: ConvConfig = ConvConfig(),
+                exec: ExecConfig = ExecConfig()) -> EcrMap:
+    """ecr_convert (ecr.cpp:51-97) by warp-ballot compaction on the GPU."""
+    if filter.channels != map.channels:
+        raise ShapeError(f"filter channels {filter.channels} != map channels {map.channels}")
+    od = conv_output_dims(map.width, map.height, filter.width, filter.height, cfg.stride)
+    dims = EcrDims(map.width, map.height, filter.width, filter.height, cfg.stride, map.channels)
+    slot = dims.slot()
+    nwin = od.width * od.height
+    ptr = np.empty(nwin, np.int32)
+    offsets = np.empty(nwin * slot, np.int32)
+    f_data = np.empty(nwin * slot, np.float32)
+    k_data = np.empty(nwin * slot, np.float32)
+    ctx = _ctx(exec)
+    nat.check(nat.lib().sconv_cu_ecr_convert(
+        ctx.handle, _ptr(map.values), map.channels, map.height, map.width, _ptr(filter.weights),
+        filter.height, filter.width, cfg.stride, _ptr(ptr), _ptr(offsets), _ptr(f_data),
+        _ptr(k_data), _flags(exec)), ctx.handle)
+    rows = []
+    row = od.width * slot
+    for b in range(od.height):
+        rows.append(EcrBlockRow(f_data[b * row:(b + 1) * row], k_data[b * row:(b + 1) * row],
+                                offsets[b * row:(b + 1) * row],
+                                ptr[b * od.width:(b + 1) * od.width]))
+    return EcrMap(dims, rows)
+
+
+def _check_ecr(ecr: EcrMap) -> None:
+    """Structural half of check_ecr (ecr.cpp:22-42); ptr ranges are checked
+    by the library."""
+    d = ecr.dims
+    threads, slot = d.out_w(), d.slot()
+    if len(ecr.block_rows) != d.out_h():
+        raise FormatError("block row count does not match output height")
+    want = threads * slot
+    for r in ecr.block_rows:
+        if (len(r.f_data) != want or len(r.k_data) != want or len(r.offsets) != want or
+                len(r.ptr) != threads):
+            raise FormatError("block row arrays do not match thread count")
+
+
+def ecr_spmv_conv(ecr: EcrMap, counters: Optional[OpCount] = None,
+                  exec: ExecConfig = ExecConfig()) -> FeatureMap:
+    """ecr_spmv_conv (ecr.cpp:99-128) on the GPU."""
+    _check_ecr(ecr)
+    d = ecr.dims
+    oh, ow, slot = d.out_h(), d.out_w(), d.slot()
+    ptr = np.ascontiguousarray(np.concatenate([r.ptr for r in ecr.block_rows]), np.int32)
+    f = np.ascontiguousarray(np.concatenate([r.f_data for r in ecr.block_rows]), np.float32)
+    k = np.ascontiguousarray(np.concatenate([r.k_data for r in ecr.block_rows]), np.float32)
+    out = np.empty(oh * ow, np.float32)
+    m, a = C.c_uint64(0), C.c_uint64(0)
+    ctx = _ctx(exec)
+    nat.check(nat.lib().sconv_cu_ecr_spmv(ctx.handle, _ptr(ptr), _ptr(f), _ptr(k), oh, ow, slot,
+                                          _ptr(out), C.byref(m), C.byref(a), _flags(exec)),
+              ctx.handle)
+    if counters is not None:
+        counters.merge(OpCount(m.value, a.value))
+    return FeatureMap(1, oh, ow, out)
+
+
+def ecr_window(ecr: EcrMap, block: int, thread: int) -> np.ndarray:
+    """Scatter one window's nonzeros back to a dense slot (ecr.cpp:130-144)."""
+    d = ecr.dims
+    if block < 0 or block >= d.out_h() or thread < 0 or thread >= d.out_w():
+        raise ShapeError("window index out of range")
+    row = ecr.block_rows[block]
+    slot = d.slot()
+    base = thread * slot
+    window = np.zeros(slot, np.float32)
+    nnz = 0 if row.ptr[thread] == -1 else int(row.ptr[thread])
+    window[row.offsets[base:base + nnz]] = row.f_data[base:base + nnz]
+    return window
+
+
+# ---------------------------------------------------------------------------
+# PECR two-phase API
+# ---------------------------------------------------------------------------
+
+
+def pecr_convert(map: FeatureMap, filter: Filter, conv: ConvConfig, pool: PoolConfig,
+                 exec: ExecConfig = ExecConfig()) -> PecrMap:
+    """pecr_convert (pecr.cpp:83-131): count pass, exclusive scan, fill pass."""
+    if filter.channels != map.channels:
+        raise ShapeError(f"filter channels {filter.channels} != map channels {map.channels}")
+    conv_output_dims(map.width, map.height, filter.width, filter.height, conv.stride)
+    pw = pecr_pack_count(map.width, filter.width, conv.stride, pool.width, pool.stride)
+    ph = pecr_pack_count(map.height, filter.height, conv.stride, pool.height, pool.stride)
+    wpp = pool.width * pool.height
+    count = np.empty(ph * pw * wpp, np.int32)
+    start = np.empty(ph * pw + 1, np.int64)
+    total = C.c_int64(0)
+    ctx = _ctx(exec)
+    L = nat.lib()
+    args = (ctx.handle, _ptr(map.values), map.channels, map.height, map.width, filter.height,
+            filter.width, conv.stride, pool.width, pool.height, pool.stride)
+    nat.check(L.sconv_cu_pecr_count(*args, _ptr(count), _ptr(start), C.byref(total),
+                                    _flags(exec)), ctx.handle)
+    t = total.value
+    data = np.empty(max(t, 1), np.float32)
+    index = np.empty(max(t, 1), np.int32)
+    nat.check(L.sconv_cu_pecr_fill(*args, _ptr(start), t, _ptr(data), _ptr(index), _flags(exec)),
+              ctx.handle)
+    dims = PecrDims(map.width, map.height, filter.width, filter.height, conv.stride, map.channels,
+                    PoolConfig(pool.width, pool.height, pool.stride, PoolMode(pool.mode)))
+    rows = []
+    for b in range(ph):
+        row = []
+        for t_ in range(pw):
+            pk = b * pw + t_
+            s, e = int(start[pk]), int(start[pk + 1])
+            row.append(PecrPoolPack(data[s:e].copy(), index[s:e].copy(),
+                                    count[pk * wpp:(pk + 1) * wpp].copy()))
+        rows.append(row)
+    return PecrMap(dims, filter.weights.copy(), rows)
+
+
+def pecr_conv_pool(pecr: PecrMap, counters: Optional[OpCount] = None,
+                   exec: ExecConfig = ExecConfig()) -> FeatureMap:
+    """pecr_conv_pool (pecr.cpp:133-172): fused conv + ReLU + pool over a PecrMap."""
+    d = pecr.dims
+    packs_w = pecr_pack_count(d.in_w, d.k_w, d.conv_stride, d.pool.width, d.pool.stride)
+    packs_h = pecr_pack_count(d.in_h, d.k_h, d.conv_stride, d.pool.height, d.pool.stride)
+    if pecr.packs_h() != packs_h:  # check_pecr, pecr.cpp:24-58
+        raise FormatError("pack row count mismatch")
+    cap = d.channels * d.k_h * d.k_w
+    if len(pecr.kernel) != cap:
+        raise FormatError("kernel length does not match dims")
+    wpp = d.windows_per_pack()
+    counts, datas, idxs, start = [], [], [], [0]
+    for row in pecr.pool_rows:
+        if len(row) != packs_w:
+            raise FormatError("pack count mismatch")
+        for pack in row:
+            if len(pack.count) != wpp:
+                raise FormatError("count length does not match windows per pack")
+            if len(pack.data) != len(pack.index):
+                raise FormatError("data/index length inconsistent with counts")
+            counts.append(np.asarray(pack.count, np.int32))
+            datas.append(np.asarray(pack.data, np.float32))
+            idxs.append(np.asarray(pack.index, np.int32))
+            start.append(start[-1] + len(pack.data))
+    count = np.ascontiguousarray(np.concatenate(counts), np.int32)
+    data = np.ascontiguousarray(np.concatenate(datas + [np.zeros(1, np.float32)]), np.float32)
+    index = np.ascontiguousarray(np.concatenate(idxs + [np.zeros(1, np.int32)]), np.int32)
+    start = np.asarray(start, np.int64)
+    kernel = np.ascontiguousarray(pecr.kernel, np.float32)
+    out = np.empty(packs_h * packs_w, np.float32)
+    m, a = C.c_uint64(0), C.c_uint64(0)
+    ctx = _ctx(exec)
+    nat.check(nat.lib().sconv_cu_pecr_pool(
+        ctx.handle, _ptr(count), _ptr(start), _ptr(data), _ptr(index), int(start[-1]),
+        _ptr(kernel), d.channels, d.k_h, d.k_w, packs_h, packs_w, d.pool.width, d.pool.height,
+        int(d.pool.mode), _ptr(out), C.byref(m), C.byref(a), _flags(exec)), ctx.handle)
+    if counters is not None:
+        counters.merge(OpCount(m.value, a.value))
+    return FeatureMap(1, packs_h, packs_w, out)
+
+
+def pecr_window(pecr: PecrMap, pack_row: int, pack_col: int, n: int) -> np.ndarray:
+    """Reconstruct window n of a pack (pecr.cpp:174-189)."""
+    d = pecr.dims
+    if (pack_row < 0 or pack_row >= pecr.packs_h() or pack_col < 0 or
+            pack_col >= pecr.packs_w() or n < 0 or n >= d.windows_per_pack()):
+        raise ShapeError("pack window index out of range")
+    pack = pecr.pool_rows[pack_row][pack_col]
+    pos = int(np.sum(pack.count[:n]))
+    window = np.zeros(d.channels * d.k_h * d.k_w, np.float32)
+    cn = int(pack.count[n])
+    window[pack.index[pos:pos + cn]] = pack.data[pos:pos + cn]
+    return window
+
+
+# ---------------------------------------------------------------------------
+# batched fused entries (the hot path)
+# ---------------------------------------------------------------------------
+
+
+def _is_torch_cuda(t) -> bool:
+    return hasattr(t, "is_cuda") and bool(getattr(t, "is_cuda"))
+
+
+def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, counters,
+             device: Optional[int], generic: bool, out, sync: bool):
+    L = nat.lib()
+    flags = (nat.F_FAST if fast else 0) | (nat.F_GENERIC if generic else 0)
+    if _is_torch_cuda(x):
+        import torch
+        if not (_is_torch_cuda(filters) and x.dtype == torch.float32 and filters.dtype == torch.float32):
+            raise ShapeError("x and filters must both be float32 CUDA tensors")
+        dev = x.device.index if device is None else device
+        x = x.contiguous()
+        filters = filters.contiguous()
+        N, Cc, H, W = x.shape
+        K, Cf, kh, kw = filters.shape
+        if Cf != Cc:
+            raise ShapeError(f"filter channels {Cf} != map channels {Cc}")
+        if kind == "ecr":
+            od = conv_output_dims(W, H, kw, kh, stride)
+            shape = (N, K, od.height, od.width)
+        else:
+            pw = pecr_pack_count(W, kw, stride, pool[0], pool[2])
+            ph = pecr_pack_count(H, kh, stride, pool[1], pool[2])
+            shape = (N, K, ph, pw)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float32, device=x.device)
+        elif tuple(out.shape) != shape or not out.is_contiguous():
+            raise ShapeError("out has the wrong shape")
+        ctx = nat.context(dev)
+        ctx.set_stream(torch.cuda.current_stream(x.device).cuda_stream)
+        flags |= nat.F_DEVICE
+        if not sync and counters is None:
+            flags |= nat.F_ASYNC
+        xp, wp, yp = x.data_ptr(), filters.data_ptr(), out.data_ptr()
+    else:
+        x = np.ascontiguousarray(x, np.float32)
+        filters = np.ascontiguousarray(filters, np.float32)
+        N, Cc, H, W = x.shape
+        K, Cf, kh, kw = filters.shape
+        if Cf != Cc:
+            raise ShapeError(f"filter channels {Cf} != map channels {Cc}")
+        if kind == "ecr":
+            od = conv_output_dims(W, H, kw, kh, stride)
+            shape = (N, K, od.height, od.width)
+        else:
+            pw = pecr_pack_count(W, kw, stride, pool[0], pool[2])
+            ph = pecr_pack_count(H, kh, stride, pool[1], pool[2])
+            shape = (N, K, ph, pw)
+        if out is None:
+            out = np.empty(shape, np.float32)
+        ctx = nat.context(0 if device is None else device)
+        xp, wp, yp = _ptr(x), _ptr(filters), _ptr(out)
+    m, a = C.c_uint64(0), C.c_uint64(0)
+    mp = C.byref(m) if counters is not None else None
+    ap = C.byref(a) if counters is not None else None
+    if kind == "ecr":
+        st = L.sconv_cu_ecr_conv(ctx.handle, xp, N, Cc, H, W, wp, K, kh, kw, stride, yp, mp, ap,
+                                 flags)
+    else:
+        st = L.sconv_cu_pecr_conv_pool(ctx.handle, xp, N, Cc, H, W, wp, K, kh, kw, stride,
+                                       pool[0], pool[1], pool[2], int(mode), yp, mp, ap, flags)
+    nat.check(st, ctx.handle)
+    if counters is not None:
+        counters.merge(OpCount(m.value, a.value))
+    return out
+
+
+def ecr_conv_batched(x, filters, stride: int = 1, *, fast: bool = False,
+                     counters: Optional[OpCount] = None, device: Optional[int] = None,
+                     generic: bool = False, out=None, sync: bool = True):
+    """Fused ECR convolution of x [N,C,H,W] by filters [K,C,kh,kw] -> [N,K,oh,ow].
+
+    Equivalent to multichannel_conv(map, filters, {stride}, Method::kEcr) per
+    image (pipeline.cpp:191-210).  numpy in -> numpy out (host copies inside);
+    torch CUDA tensors in -> torch out on the current stream.
+    """
+    return _batched("ecr", x, filters, stride, None, 0, fast, counters, device, generic, out,
+                    sync)
+
+
+def pecr_conv_pool_batched(x, filters, stride: int = 1, pool: PoolConfig = PoolConfig(2, 2, 2),
+                           *, fast: bool = False, counters: Optional[OpCount] = None,
+                           device: Optional[int] = None, generic: bool = False, out=None,
+                           sync: bool = True):
+    """Fused conv + ReLU + pooling (forward's fused branch, pipeline.cpp:249-264)."""
+    return _batched("pecr", x, filters, stride, (pool.width, pool.height, pool.stride),
+                    int(pool.mode), fast, counters, device, generic, out, sync)
+
+
+def multichannel_conv(map: FeatureMap, filters: Sequence[Filter], cfg: ConvConfig,
+                      method: str = "ecr", exec: ExecConfig = ExecConfig(),
+                      counters: Optional[OpCount] = None) -> FeatureMap:
+    """GPU multichannel_conv (pipeline.cpp:191-210) for Method::kEcr: all K
+    filters in one fused launch, output stacked K x oh x ow."""
+    if not filters:
+        raise ConfigError("multichannel_conv requires filters")
+    if method != "ecr":
+        raise ConfigError("multichannel_conv on the GPU supports the ecr method only")
+    for f in filters:
+        if f.channels != map.channels:
+            raise ShapeError(f"filter channels {f.channels} != map channels {map.channels}")
+        if (f.height, f.width) != (filters[0].height, filters[0].width):
+            raise ShapeError("filters must share dims")
+    if exec.workers < 1:
+        raise ConfigError("workers must be >= 1")
+    w = np.stack([f.array() for f in filters])
+    y = ecr_conv_batched(map.array()[None], w, cfg.stride, fast=exec.fast, counters=counters,
+                         device=exec.device)
+    return FeatureMap(len(filters), y.shape[2], y.shape[3], y.reshape(-1))
+
+
+# ---------------------------------------------------------------------------
+# datasets / reports / planning
+# ---------------------------------------------------------------------------
+
+
+def generate(height: int, width: int, channels: int, sparsity: float, seed: int) -> FeatureMap:
+    """sconv::generate (dataset.cpp:77-100), bit-identical."""
+    if not (0.0 <= sparsity <= 1.0):
+        raise ConfigError(f"sparsity must be in [0, 1], got {sparsity}")
+    _check_dims(channels, height, width, "feature map")
+    out = np.empty(channels * height * width, np.float32)
+    nat.check(nat.lib().sconv_generate(height, width, channels, float(sparsity), seed, _ptr(out)))
+    return FeatureMap(channels, height, width, out)
+
+
+def generate_batch(seeds: Sequence[int], height: int, width: int, channels: int,
+                   sparsity: float, threads: int = 0, out: Optional[np.ndarray] = None) -> np.ndarray:
+    """maps[i] = generate(height, width, channels, sparsity, seeds[i]) -> [N,C,H,W]."""
+    seeds = np.ascontiguousarray(seeds, np.uint64)
+    n = len(seeds)
+    if out is None:
+        out = np.empty((n, channels, height, width), np.float32)
+    nat.check(nat.lib().sconv_generate_batch(n, height, width, channels, float(sparsity),
+                                             _ptr(seeds), _ptr(out), threads))
+    return out
+
+
+def checksum_hex(values) -> str:
+    """checksum_hex (report.cpp:14-30)."""
+    v = np.ascontiguousarray(values, np.float32).reshape(-1)
+    return "%016x" % nat.lib().sconv_checksum(_ptr(v), v.size)
+
+
+def launch_plan(n, c, h, w, k, kh, kw, stride, pool: Optional[PoolConfig] = None,
+                fast: bool = False) -> dict:
+    p = nat.LaunchPlan()
+    pw, ph, ps = (pool.width, pool.height, pool.stride) if pool else (0, 0, 1)
+    nat.check(nat.lib().sconv_cu_plan(n, c, h, w, k, kh, kw, stride, pw, ph, ps,
+                                      nat.F_FAST if fast else 0, C.byref(p)))
+    return {f: getattr(p, f) for f, _ in nat.LaunchPlan._fields_}
+
+
+def shard(n: int, k: int, world: int, rank: int):
+    """sconv_shard: (n_begin, n_end, k_begin, k_end) of `rank`."""
+    v = [C.c_int() for _ in range(4)]
+    nat.check(nat.lib().sconv_shard(n, k, world, rank, *[C.byref(t) for t in v]))
+    return tuple(t.value for t in v)

@@ -1,0 +1,80 @@
+// common.cuh -- small device helpers shared by the sconv sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sconv_cu {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// One multiply-accumulate term.  EXACT mode reproduces the reference's x86-64
+// arithmetic (`acc += a*b` compiled without FMA: rounded product, rounded
+// sum -- src/ecr.cpp:117-120, src/pecr.cpp:152-155).  FAST mode contracts the
+// term into a single FFMA.
+template <bool FAST>
+__device__ __forceinline__ float mac(float acc, float a, float b) {
+  if constexpr (FAST) {
+    return __fmaf_rn(a, b, acc);
+  } else {
+    return __fadd_rn(acc, __fmul_rn(a, b));
+  }
+}
+
+// Pooling fold of pecr_conv_pool (src/pecr.cpp:147-167).
+struct PoolFold {
+  float best = 0.0f;  // max mode: running max starts at +0.0 -> ReLU folded
+  float sum = 0.0f;   // mean mode: sum of max(acc, 0) in window raster order
+  __device__ __forceinline__ void add(float acc, int mode) {
+    if (mode == 0) {
+      if (acc > best) best = acc;
+    } else {
+      sum = __fadd_rn(sum, acc > 0.0f ? acc : 0.0f);
+    }
+  }
+  __device__ __forceinline__ float result(int mode, int windows) const {
+    return mode == 0 ? best : __fdiv_rn(sum, static_cast<float>(windows));
+  }
+};
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Deterministic integer reduction of a per-thread value into *dst
+// (block reduce, one 64-bit atomic per block; integer sums are order-free).
+__device__ __forceinline__ void block_add_u64(unsigned long long v, unsigned long long* dst) {
+  __shared__ unsigned long long part[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(kFull, v, o);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) part[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    v = (threadIdx.x < static_cast<unsigned>(nw)) ? part[threadIdx.x] : 0ull;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(kFull, v, o);
+    if (threadIdx.x == 0 && v) atomicAdd(dst, v);
+  }
+  __syncthreads();
+}
+
+}  // namespace sconv_cu

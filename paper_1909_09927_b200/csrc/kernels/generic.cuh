@@ -1,0 +1,88 @@
+// generic.cuh -- shape-generic ECR / PECR kernels (any kernel size, stride,
+// pooling window and pooling stride).  One thread per output; used for the
+// configurations the tiled kernel is not specialised for.  Same term order
+// and arithmetic modes as the tiled path, so EXACT stays bit-identical.
+#pragma once
+
+#include "common.cuh"
+
+namespace sconv_cu {
+
+struct GenericArgs {
+  const float* x;  // [N][C][H][W]
+  const float* w;  // [K][C][kh][kw]
+  float* y;
+  int N, C, H, W, K, kh, kw, S, OH, OW;
+  int pw, ph, ps, mode;  // PECR only
+  int PH, PW;            // PECR pack grid
+};
+
+template <bool FAST>
+__device__ __forceinline__ float window_dot(const float* xn, const float* wk, int C, int H, int W,
+                                            int kh, int kw, int y0, int x0) {
+  float acc = 0.0f;
+  for (int c = 0; c < C; ++c) {
+    const float* xc = xn + (static_cast<size_t>(c) * H + y0) * W + x0;
+    const float* wc = wk + c * kh * kw;
+    for (int i = 0; i < kh; ++i)
+      for (int j = 0; j < kw; ++j) {
+        const float v = __ldg(xc + i * W + j);
+        if (v != 0.0f) acc = mac<FAST>(acc, v, __ldg(wc + i * kw + j));
+      }
+  }
+  return acc;
+}
+
+// ECR: ecr_convert + ecr_spmv_conv per (image, filter, window).
+template <bool FAST>
+__global__ void ecr_generic_kernel(const GenericArgs a) {
+  const size_t total = static_cast<size_t>(a.N) * a.K * a.OH * a.OW;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int ox = static_cast<int>(idx % a.OW);
+    const int oy = static_cast<int>((idx / a.OW) % a.OH);
+    const int k = static_cast<int>((idx / (static_cast<size_t>(a.OW) * a.OH)) % a.K);
+    const int n = static_cast<int>(idx / (static_cast<size_t>(a.OW) * a.OH * a.K));
+    const float* xn = a.x + static_cast<size_t>(n) * a.C * a.H * a.W;
+    const float* wk = a.w + static_cast<size_t>(k) * a.C * a.kh * a.kw;
+    a.y[idx] = window_dot<FAST>(xn, wk, a.C, a.H, a.W, a.kh, a.kw, oy * a.S, ox * a.S);
+  }
+}
+
+// PECR: pack (b, t) folds windows n = 0 .. pw*ph-1 in raster order, window n
+// at (b*cs*ps + (n/pw)*cs, t*cs*ps + (n%pw)*cs) -- src/pecr.cpp:106-112.
+template <bool FAST>
+__global__ void pecr_generic_kernel(const GenericArgs a) {
+  const size_t total = static_cast<size_t>(a.N) * a.K * a.PH * a.PW;
+  const int wpp = a.pw * a.ph;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(idx % a.PW);
+    const int b = static_cast<int>((idx / a.PW) % a.PH);
+    const int k = static_cast<int>((idx / (static_cast<size_t>(a.PW) * a.PH)) % a.K);
+    const int n = static_cast<int>(idx / (static_cast<size_t>(a.PW) * a.PH * a.K));
+    const float* xn = a.x + static_cast<size_t>(n) * a.C * a.H * a.W;
+    const float* wk = a.w + static_cast<size_t>(k) * a.C * a.kh * a.kw;
+    PoolFold f;
+    for (int q = 0; q < wpp; ++q) {
+      const int wy = b * a.S * a.ps + (q / a.pw) * a.S;
+      const int wx = t * a.S * a.ps + (q % a.pw) * a.S;
+      f.add(window_dot<FAST>(xn, wk, a.C, a.H, a.W, a.kh, a.kw, wy, wx), a.mode);
+    }
+    a.y[idx] = f.result(a.mode, wpp);
+  }
+}
+
+// Filter re-layout for the tiled kernel: wt[c][i*kw+j][k] = w[k][c][i][j].
+__global__ void transpose_filters_kernel(const float* __restrict__ w, float* __restrict__ wt, int K,
+                                         int C, int KK) {
+  const size_t total = static_cast<size_t>(K) * C * KK;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(idx % K);
+    const size_t cij = idx / K;  // c*KK + ij
+    wt[idx] = __ldg(w + static_cast<size_t>(k) * C * KK + cij);
+  }
+}
+
+}  // namespace sconv_cu

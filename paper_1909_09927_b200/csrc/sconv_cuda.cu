@@ -1,0 +1,794 @@
+// sconv_cuda.cu -- C ABI of libsconv_cuda.so (declared in include/sconv_cuda.h).
+//
+// Host launch / partition layer: argument validation with the reference's
+// error taxonomy, per-context stream + workspace, host<->device staging for
+// host-pointer calls, kernel selection, and the multi-GPU shard driver.  It
+// replaces plan()/dispatch() (src/exec.cpp:8-36, include/sconv/exec.hpp:57-120)
+// for the ECR / PECR entry points.
+#include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "kernels/ecr_tiled.cuh"
+#include "kernels/format.cuh"
+#include "kernels/generic.cuh"
+#include "sconv_cuda.h"
+
+using namespace sconv_cu;
+
+struct sconv_cu_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+  char* ws = nullptr;
+  size_t ws_cap = 0;
+  int num_sms = 148;
+  int smem_optin = 0;
+};
+
+namespace {
+
+thread_local std::string g_noctx_err;
+
+int fail(sconv_cu_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  (ctx ? ctx->err : g_noctx_err) = buf;
+  return code;
+}
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, SCONV_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+#define TRY(expr)                 \
+  do {                            \
+    const int rc_ = (expr);       \
+    if (rc_ != SCONV_OK) return rc_; \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Bump allocator over the context workspace (grown on demand; growth drains
+// the stream first because queued work may still read the old buffer).
+struct Arena {
+  sconv_cu_ctx* ctx;
+  std::vector<size_t> sizes;
+  size_t add(size_t bytes) {
+    sizes.push_back((bytes + 255) & ~size_t{255});
+    return sizes.size() - 1;
+  }
+  int commit(std::vector<char*>& out) {
+    size_t total = 0;
+    for (size_t s : sizes) total += s;
+    if (total > ctx->ws_cap) {
+      const size_t cap = std::max(total, ctx->ws_cap + ctx->ws_cap / 2);
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (ctx->ws) CK(cudaFree(ctx->ws));
+      ctx->ws = nullptr;
+      ctx->ws_cap = 0;
+      CK(cudaMalloc(&ctx->ws, cap));
+      ctx->ws_cap = cap;
+    }
+    out.clear();
+    size_t off = 0;
+    for (size_t s : sizes) {
+      out.push_back(ctx->ws + off);
+      off += s;
+    }
+    return SCONV_OK;
+  }
+};
+
+int conv_dims(sconv_cu_ctx* ctx, int w, int h, int kw, int kh, int stride, int* ow, int* oh) {
+  // conv_output_dims, src/tensor.cpp:44-55
+  if (w < 1 || h < 1 || kw < 1 || kh < 1) return fail(ctx, SCONV_ERR_SHAPE, "dims must be positive");
+  if (stride < 1) return fail(ctx, SCONV_ERR_CONFIG, "stride must be >= 1");
+  if (kw > w || kh > h)
+    return fail(ctx, SCONV_ERR_SHAPE, "kernel %dx%d larger than map %dx%d", kw, kh, w, h);
+  *ow = (w - kw) / stride + 1;
+  *oh = (h - kh) / stride + 1;
+  return SCONV_OK;
+}
+
+int pack_count(sconv_cu_ctx* ctx, int in, int k, int cs, int p, int ps, int* out) {
+  // Eq. 3, src/pecr.cpp:62-81
+  if (in < 1 || k < 1 || cs < 1 || p < 1 || ps < 1)
+    return fail(ctx, SCONV_ERR_CONFIG, "pack count arguments must be positive");
+  const int num = in - k + cs - cs * p + ps * cs;
+  const int den = ps * cs;
+  if (num <= 0 || num % den != 0)
+    return fail(ctx, SCONV_ERR_CONFIG,
+                "pool tiling does not divide extent %d: (%d - %d + %d - %d + %d) / %d is not a "
+                "positive integer",
+                in, in, k, cs, cs * p, den, den);
+  *out = num / den;
+  return SCONV_OK;
+}
+
+unsigned grid_for(size_t work, int threads, int num_sms) {
+  const size_t blocks = (work + threads - 1) / threads;
+  return static_cast<unsigned>(std::min<size_t>(std::max<size_t>(blocks, 1), size_t(num_sms) * 64));
+}
+
+int finish_launch(sconv_cu_ctx* ctx, const char* what) {
+  ctx->launches++;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, SCONV_ERR_CUDA, "launch %s: %s", what, cudaGetErrorString(e));
+  return SCONV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Tiled kernel registry.  Specialisations exist for the VGG / AlexNet /
+// GoogLeNet 3x3 stride-1 shapes; every other shape takes the generic kernel.
+// ---------------------------------------------------------------------------
+template <int P>
+using Cfg3x3R4 = TiledCfg<3, 3, 1, 4, 8, 4, 1, 2, 2, 8, P>;  // 8x16 outputs x 128 channels
+template <int P>
+using Cfg3x3R2 = TiledCfg<3, 3, 1, 4, 8, 2, 1, 2, 2, 8, P>;  // 8x16 outputs x 64 channels
+
+template <class Cfg, bool FAST>
+int launch_tiled_cfg(sconv_cu_ctx* ctx, const TiledArgs& a, int N) {
+  auto kern = ecr_tiled_kernel<Cfg, FAST, 2>;
+  static bool attr_done[64] = {};
+  const int slot = ctx->device & 63;
+  if (!attr_done[slot]) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_done[slot] = true;
+  }
+  const int tiles_y = (a.OH + Cfg::OTH - 1) / Cfg::OTH;
+  const int tiles_x = (a.OW + Cfg::OTW - 1) / Cfg::OTW;
+  TiledArgs b = a;
+  b.tiles_x = tiles_x;
+  dim3 grid(tiles_y * tiles_x, (a.K + Cfg::KT - 1) / Cfg::KT, N);
+  kern<<<grid, Cfg::NT, Cfg::SMEM_BYTES, ctx->stream>>>(b);
+  return finish_launch(ctx, "ecr_tiled_kernel");
+}
+
+// which tiled config (0 = none -> generic)
+int pick_tiled(int K, int kh, int kw, int S, int P) {
+  if (kh == 3 && kw == 3 && S == 1 && (P == 0 || P == 2) && K >= 32) return K % 128 == 0 ? 1 : 2;
+  return 0;
+}
+
+template <bool FAST>
+int launch_tiled(sconv_cu_ctx* ctx, int which, int P, const TiledArgs& a, int N) {
+  if (which == 1)
+    return P == 0 ? launch_tiled_cfg<Cfg3x3R4<0>, FAST>(ctx, a, N)
+                  : launch_tiled_cfg<Cfg3x3R4<2>, FAST>(ctx, a, N);
+  return P == 0 ? launch_tiled_cfg<Cfg3x3R2<0>, FAST>(ctx, a, N)
+                : launch_tiled_cfg<Cfg3x3R2<2>, FAST>(ctx, a, N);
+}
+
+template <class Cfg>
+void fill_plan(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
+  p->kernel = which;
+  p->grid_x = ((OH + Cfg::OTH - 1) / Cfg::OTH) * ((OW + Cfg::OTW - 1) / Cfg::OTW);
+  p->grid_y = (K + Cfg::KT - 1) / Cfg::KT;
+  p->grid_z = N;
+  p->block_threads = Cfg::NT;
+  p->smem_bytes = Cfg::SMEM_BYTES;
+  p->tile_h = Cfg::OTH;
+  p->tile_w = Cfg::OTW;
+  p->tile_k = Cfg::KT;
+}
+
+// Shared body of the fused ECR / PECR entries.
+int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, const float* filt,
+               int k, int kh, int kw, int stride, int pw, int ph, int ps, int mode, float* y,
+               uint64_t* muls, uint64_t* adds, unsigned flags) {
+  if (!ctx) return fail(nullptr, SCONV_ERR_ARG, "null context");
+  const bool pecr = pw > 0;
+  if (n < 0 || k < 0) return fail(ctx, SCONV_ERR_SHAPE, "negative batch or filter count");
+  if (c < 1) return fail(ctx, SCONV_ERR_SHAPE, "channels must be positive");
+  int OW, OH;
+  TRY(conv_dims(ctx, w, h, kw, kh, stride, &OW, &OH));
+  int PWo = 0, PHo = 0;
+  if (pecr) {
+    if (mode != SCONV_POOL_MAX && mode != SCONV_POOL_MEAN)
+      return fail(ctx, SCONV_ERR_CONFIG, "unknown pool mode %d", mode);
+    TRY(pack_count(ctx, w, kw, stride, pw, ps, &PWo));
+    TRY(pack_count(ctx, h, kh, stride, ph, ps, &PHo));
+  }
+  const bool dev = flags & SCONV_F_DEVICE, async = flags & SCONV_F_ASYNC, fast = flags & SCONV_F_FAST;
+  if (async && !dev) return fail(ctx, SCONV_ERR_ARG, "SCONV_F_ASYNC requires SCONV_F_DEVICE");
+  if (async && (muls || adds)) return fail(ctx, SCONV_ERR_ARG, "counters need a synchronous call");
+  if (n == 0 || k == 0) return SCONV_OK;
+  if (!x || !filt || !y) return fail(ctx, SCONV_ERR_ARG, "null tensor pointer");
+
+  const size_t x_elems = size_t(n) * c * h * w, w_elems = size_t(k) * c * kh * kw;
+  const size_t y_elems = pecr ? size_t(n) * k * PHo * PWo : size_t(n) * k * OH * OW;
+  int P = 0;
+  if (pecr && pw == ph && pw == ps) P = pw;
+  const int which = (flags & SCONV_F_GENERIC) ? 0 : pick_tiled(k, kh, kw, stride, pecr ? (P ? P : -1) : 0);
+  const bool counters = muls || adds;
+
+  DeviceGuard guard(ctx->device);
+  Arena ar{ctx, {}};
+  const size_t i_x = dev ? 0 : ar.add(x_elems * 4);
+  const size_t i_w = dev ? 0 : ar.add(w_elems * 4);
+  const size_t i_y = dev ? 0 : ar.add(y_elems * 4);
+  const size_t i_wt = which ? ar.add(w_elems * 4) : 0;
+  const size_t i_pix = counters ? ar.add(size_t(n) * h * w * 4) : 0;
+  const size_t i_ops = ar.add(64);
+  std::vector<char*> p;
+  TRY(ar.commit(p));
+  const float* dx = dev ? x : reinterpret_cast<float*>(p[i_x]);
+  const float* dw = dev ? filt : reinterpret_cast<float*>(p[i_w]);
+  float* dy = dev ? y : reinterpret_cast<float*>(p[i_y]);
+  auto* dops = reinterpret_cast<unsigned long long*>(p[i_ops]);
+  cudaStream_t st = ctx->stream;
+
+  if (!dev) {
+    CK(cudaMemcpyAsync(const_cast<float*>(dx), x, x_elems * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(const_cast<float*>(dw), filt, w_elems * 4, cudaMemcpyHostToDevice, st));
+  }
+
+  if (which) {
+    float* wt = reinterpret_cast<float*>(p[i_wt]);
+    transpose_filters_kernel<<<grid_for(w_elems, 256, ctx->num_sms), 256, 0, st>>>(dw, wt, k, c,
+                                                                                    kh * kw);
+    TRY(finish_launch(ctx, "transpose_filters_kernel"));
+    TiledArgs a{dx, wt, dy, c, h, w, k, OH, OW, 0, mode};
+    TRY(fast ? launch_tiled<true>(ctx, which, P, a, n) : launch_tiled<false>(ctx, which, P, a, n));
+  } else {
+    GenericArgs a{dx, dw, dy, n, c, h, w, k, kh, kw, stride, OH, OW, pw, ph, ps, mode, PHo, PWo};
+    const unsigned g = grid_for(y_elems, 256, ctx->num_sms);
+    if (pecr) {
+      if (fast)
+        pecr_generic_kernel<true><<<g, 256, 0, st>>>(a);
+      else
+        pecr_generic_kernel<false><<<g, 256, 0, st>>>(a);
+      TRY(finish_launch(ctx, "pecr_generic_kernel"));
+    } else {
+      if (fast)
+        ecr_generic_kernel<true><<<g, 256, 0, st>>>(a);
+      else
+        ecr_generic_kernel<false><<<g, 256, 0, st>>>(a);
+      TRY(finish_launch(ctx, "ecr_generic_kernel"));
+    }
+  }
+
+  if (counters) {
+    int32_t* pix = reinterpret_cast<int32_t*>(p[i_pix]);
+    CK(cudaMemsetAsync(dops, 0, 16, st));
+    pixel_nnz_kernel<<<grid_for(size_t(n) * h * w, 256, ctx->num_sms), 256, 0, st>>>(dx, n, c, h, w,
+                                                                                    pix);
+    TRY(finish_launch(ctx, "pixel_nnz_kernel"));
+    OpsArgs oa{pix, n, h, w, kh, kw, stride, OH, OW, PHo, PWo, pecr ? pw : 0, ph, ps, dops};
+    const size_t items = pecr ? size_t(n) * PHo * PWo : size_t(n) * OH * OW;
+    ops_kernel<<<grid_for(items, 256, ctx->num_sms), 256, 0, st>>>(oa);
+    TRY(finish_launch(ctx, "ops_kernel"));
+    unsigned long long hops[2];
+    CK(cudaMemcpyAsync(hops, dops, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    // nnz is filter independent: every filter sees the same windows
+    if (muls) *muls += hops[0] * static_cast<uint64_t>(k);
+    if (adds) *adds += hops[1] * static_cast<uint64_t>(k);
+  }
+  if (!dev) CK(cudaMemcpyAsync(y, dy, y_elems * 4, cudaMemcpyDeviceToHost, st));
+  if (!async) CK(cudaStreamSynchronize(st));
+  return SCONV_OK;
+}
+
+template <typename F>
+int run_multi(sconv_cu_ctx** ctxs, int nctx, int n, int k, size_t in_per_img, size_t w_per_filt,
+              size_t out_per_map, const float* x, const float* filters, float* y, uint64_t* muls,
+              uint64_t* adds, F&& call) {
+  if (!ctxs || nctx < 1) return fail(nullptr, SCONV_ERR_ARG, "no contexts");
+  std::vector<int> rc(nctx, SCONV_OK);
+  std::vector<uint64_t> m(nctx, 0), a(nctx, 0);
+  std::vector<std::vector<float>> tmp(nctx);
+  std::vector<std::thread> pool;
+  for (int r = 0; r < nctx; ++r) {
+    pool.emplace_back([&, r] {
+      int n0, n1, k0, k1;
+      sconv_shard(n, k, nctx, r, &n0, &n1, &k0, &k1);
+      if (n1 <= n0 || k1 <= k0) return;
+      const bool ksplit = (k1 - k0) != k;
+      float* out = y + size_t(n0) * k * out_per_map;
+      if (ksplit) {
+        tmp[r].resize(size_t(n1 - n0) * (k1 - k0) * out_per_map);
+        out = tmp[r].data();
+      }
+      rc[r] = call(ctxs[r], x + size_t(n0) * in_per_img, n1 - n0, filters + size_t(k0) * w_per_filt,
+                   k1 - k0, out, (muls ? &m[r] : nullptr), (adds ? &a[r] : nullptr));
+      if (rc[r] == SCONV_OK && ksplit) {
+        for (int i = 0; i < n1 - n0; ++i)
+          std::memcpy(y + (size_t(n0 + i) * k + k0) * out_per_map,
+                      tmp[r].data() + size_t(i) * (k1 - k0) * out_per_map,
+                      size_t(k1 - k0) * out_per_map * 4);
+      }
+    });
+  }
+  for (auto& t : pool) t.join();
+  for (int r = 0; r < nctx; ++r)
+    if (rc[r] != SCONV_OK) {
+      g_noctx_err = ctxs[r]->err;
+      return rc[r];
+    }
+  for (int r = 0; r < nctx; ++r) {
+    if (muls) *muls += m[r];
+    if (adds) *adds += a[r];
+  }
+  return SCONV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sconv_cu_version(void) { return "sconv_cuda 1 (sm_100a)"; }
+
+int sconv_cu_device_count(int* count) {
+  if (!count) return SCONV_ERR_ARG;
+  const cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(nullptr, SCONV_ERR_CUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  return SCONV_OK;
+}
+
+int sconv_cu_ctx_create(int device, sconv_cu_ctx** out) {
+  if (!out) return SCONV_ERR_ARG;
+  *out = nullptr;
+  sconv_cu_ctx* ctx = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || device < 0 || device >= ndev)
+    return fail(nullptr, SCONV_ERR_CUDA, "no CUDA device %d (%s)", device,
+                e != cudaSuccess ? cudaGetErrorString(e) : "out of range");
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return fail(nullptr, SCONV_ERR_CUDA, "%s", cudaGetErrorString(e));
+  if (prop.major != 10)
+    return fail(nullptr, SCONV_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a",
+                device, prop.major, prop.minor);
+  ctx = new sconv_cu_ctx();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  ctx->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
+  DeviceGuard guard(device);
+  e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return fail(nullptr, SCONV_ERR_CUDA, "%s", cudaGetErrorString(e));
+  }
+  ctx->stream = ctx->own;
+  *out = ctx;
+  return SCONV_OK;
+}
+
+int sconv_cu_ctx_destroy(sconv_cu_ctx* ctx) {
+  if (!ctx) return SCONV_ERR_ARG;
+  {
+    DeviceGuard guard(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+  }
+  delete ctx;
+  return SCONV_OK;
+}
+
+int sconv_cu_ctx_set_stream(sconv_cu_ctx* ctx, void* stream) {
+  if (!ctx) return SCONV_ERR_ARG;
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));  // workspace is stream-ordered
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  return SCONV_OK;
+}
+
+void* sconv_cu_ctx_stream(sconv_cu_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+int sconv_cu_ctx_device(sconv_cu_ctx* ctx) { return ctx ? ctx->device : -1; }
+
+int sconv_cu_synchronize(sconv_cu_ctx* ctx) {
+  if (!ctx) return SCONV_ERR_ARG;
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SCONV_OK;
+}
+
+const char* sconv_cu_last_error(const sconv_cu_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_noctx_err.c_str();
+}
+
+uint64_t sconv_cu_launch_count(const sconv_cu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int sconv_conv_output_dims(int in_w, int in_h, int k_w, int k_h, int stride, int* out_w,
+                           int* out_h) {
+  if (!out_w || !out_h) return SCONV_ERR_ARG;
+  return conv_dims(nullptr, in_w, in_h, k_w, k_h, stride, out_w, out_h);
+}
+
+int sconv_pecr_pack_count(int in_extent, int k_extent, int conv_stride, int pool_extent,
+                          int pool_stride, int* packs) {
+  if (!packs) return SCONV_ERR_ARG;
+  return pack_count(nullptr, in_extent, k_extent, conv_stride, pool_extent, pool_stride, packs);
+}
+
+int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride, int pool_w,
+                  int pool_h, int pool_stride, unsigned flags, sconv_launch_plan* out) {
+  if (!out) return SCONV_ERR_ARG;
+  std::memset(out, 0, sizeof(*out));
+  if (c < 1) return fail(nullptr, SCONV_ERR_SHAPE, "channels must be positive");
+  int OW, OH;
+  TRY(conv_dims(nullptr, w, h, kw, kh, stride, &OW, &OH));
+  int P = 0, PWo = OW, PHo = OH;
+  if (pool_w > 0) {
+    TRY(pack_count(nullptr, w, kw, stride, pool_w, pool_stride, &PWo));
+    TRY(pack_count(nullptr, h, kh, stride, pool_h, pool_stride, &PHo));
+    P = (pool_w == pool_h && pool_w == pool_stride) ? pool_w : -1;
+  }
+  const int which = (flags & SCONV_F_GENERIC) ? 0 : pick_tiled(k, kh, kw, stride, P);
+  if (which == 1) {
+    fill_plan<Cfg3x3R4<0>>(out, which, n, k, OH, OW);
+  } else if (which == 2) {
+    fill_plan<Cfg3x3R2<0>>(out, which, n, k, OH, OW);
+  } else {
+    const size_t work = size_t(n) * k * PHo * PWo;
+    out->kernel = 0;
+    out->grid_x = static_cast<int>(grid_for(work, 256, 148));
+    out->grid_y = out->grid_z = 1;
+    out->block_threads = 256;
+    out->tile_h = out->tile_w = out->tile_k = 1;
+  }
+  return SCONV_OK;
+}
+
+int sconv_cu_ecr_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w,
+                      const float* filters, int k, int kh, int kw, int stride, float* y,
+                      uint64_t* muls, uint64_t* adds, unsigned flags) {
+  return fused_conv(ctx, x, n, c, h, w, filters, k, kh, kw, stride, 0, 0, 1, 0, y, muls, adds,
+                    flags);
+}
+
+int sconv_cu_pecr_conv_pool(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w,
+                            const float* filters, int k, int kh, int kw, int stride, int pool_w,
+                            int pool_h, int pool_stride, int mode, float* y, uint64_t* muls,
+                            uint64_t* adds, unsigned flags) {
+  if (pool_w < 1 || pool_h < 1)
+    return fail(ctx, SCONV_ERR_CONFIG, "pack count arguments must be positive");
+  return fused_conv(ctx, x, n, c, h, w, filters, k, kh, kw, stride, pool_w, pool_h, pool_stride,
+                    mode, y, muls, adds, flags);
+}
+
+int sconv_cu_ecr_convert(sconv_cu_ctx* ctx, const float* x, int c, int h, int w,
+                         const float* filter, int kh, int kw, int stride, int32_t* ptr,
+                         int32_t* offsets, float* f_data, float* k_data, unsigned flags) {
+  if (!ctx) return fail(nullptr, SCONV_ERR_ARG, "null context");
+  if (c < 1) return fail(ctx, SCONV_ERR_SHAPE, "channels must be positive");
+  int OW, OH;
+  TRY(conv_dims(ctx, w, h, kw, kh, stride, &OW, &OH));
+  if (!x || !filter || !ptr || !offsets || !f_data || !k_data)
+    return fail(ctx, SCONV_ERR_ARG, "null pointer");
+  const bool dev = flags & SCONV_F_DEVICE;
+  const size_t nwin = size_t(OH) * OW, slot = size_t(c) * kh * kw;
+  DeviceGuard guard(ctx->device);
+  Arena ar{ctx, {}};
+  const size_t ix = dev ? 0 : ar.add(size_t(c) * h * w * 4), iw = dev ? 0 : ar.add(slot * 4);
+  const size_t ip = dev ? 0 : ar.add(nwin * 4), io = dev ? 0 : ar.add(nwin * slot * 4);
+  const size_t iff = dev ? 0 : ar.add(nwin * slot * 4), ik = dev ? 0 : ar.add(nwin * slot * 4);
+  std::vector<char*> p;
+  TRY(ar.commit(p));
+  cudaStream_t st = ctx->stream;
+  EcrExportArgs a{x, filter, c, h, w, kh, kw, stride, OH, OW, ptr, offsets, f_data, k_data};
+  if (!dev) {
+    a.x = reinterpret_cast<float*>(p[ix]);
+    a.filter = reinterpret_cast<float*>(p[iw]);
+    a.ptr = reinterpret_cast<int32_t*>(p[ip]);
+    a.offsets = reinterpret_cast<int32_t*>(p[io]);
+    a.f_data = reinterpret_cast<float*>(p[iff]);
+    a.k_data = reinterpret_cast<float*>(p[ik]);
+    CK(cudaMemcpyAsync(const_cast<float*>(a.x), x, size_t(c) * h * w * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(const_cast<float*>(a.filter), filter, slot * 4, cudaMemcpyHostToDevice, st));
+  }
+  ecr_export_kernel<<<grid_for(nwin * 32, 256, 1 << 20), 256, 0, st>>>(a);
+  TRY(finish_launch(ctx, "ecr_export_kernel"));
+  if (!dev) {
+    CK(cudaMemcpyAsync(ptr, a.ptr, nwin * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(offsets, a.offsets, nwin * slot * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(f_data, a.f_data, nwin * slot * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(k_data, a.k_data, nwin * slot * 4, cudaMemcpyDeviceToHost, st));
+  }
+  if (!(flags & SCONV_F_ASYNC)) CK(cudaStreamSynchronize(st));
+  return SCONV_OK;
+}
+
+int sconv_cu_ecr_spmv(sconv_cu_ctx* ctx, const int32_t* ptr, const float* f_data,
+                      const float* k_data, int oh, int ow, int slot, float* y, uint64_t* muls,
+                      uint64_t* adds, unsigned flags) {
+  if (!ctx) return fail(nullptr, SCONV_ERR_ARG, "null context");
+  if (oh < 1 || ow < 1 || slot < 1) return fail(ctx, SCONV_ERR_FORMAT, "empty ECR geometry");
+  if (!ptr || !f_data || !k_data || !y) return fail(ctx, SCONV_ERR_ARG, "null pointer");
+  const bool dev = flags & SCONV_F_DEVICE, fast = flags & SCONV_F_FAST;
+  const size_t nwin = size_t(oh) * ow;
+  if (!dev) {  // check_ecr ptr range on the host copy (src/ecr.cpp:32-38)
+    for (size_t i = 0; i < nwin; ++i)
+      if (ptr[i] < -1 || ptr[i] > slot)
+        return fail(ctx, SCONV_ERR_FORMAT, "corrupted ptr value %d outside [-1, %d]", ptr[i], slot);
+  }
+  DeviceGuard guard(ctx->device);
+  Arena ar{ctx, {}};
+  const size_t ip = dev ? 0 : ar.add(nwin * 4), iff = dev ? 0 : ar.add(nwin * slot * 4);
+  const size_t ik = dev ? 0 : ar.add(nwin * slot * 4), iy = dev ? 0 : ar.add(nwin * 4);
+  const size_t iops = ar.add(64);
+  std::vector<char*> p;
+  TRY(ar.commit(p));
+  cudaStream_t st = ctx->stream;
+  auto* ops = reinterpret_cast<unsigned long long*>(p[iops]);
+  EcrSpmvArgs a{ptr, f_data, k_data, static_cast<int>(nwin), slot, y, ops,
+                reinterpret_cast<int*>(ops + 2)};
+  if (!dev) {
+    a.ptr = reinterpret_cast<int32_t*>(p[ip]);
+    a.f_data = reinterpret_cast<float*>(p[iff]);
+    a.k_data = reinterpret_cast<float*>(p[ik]);
+    a.y = reinterpret_cast<float*>(p[iy]);
+    CK(cudaMemcpyAsync(const_cast<int32_t*>(a.ptr), ptr, nwin * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(const_cast<float*>(a.f_data), f_data, nwin * slot * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(const_cast<float*>(a.k_data), k_data, nwin * slot * 4, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemsetAsync(ops, 0, 24, st));
+  if (fast) {
+    ecr_spmv_fast_kernel<<<grid_for(nwin * 32, 256, 1 << 20), 256, 0, st>>>(a);
+  } else {
+    ecr_spmv_exact_kernel<<<grid_for(nwin, 256, 1 << 20), 256, 0, st>>>(a);
+  }
+  TRY(finish_launch(ctx, "ecr_spmv_kernel"));
+  unsigned long long h[3];
+  CK(cudaMemcpyAsync(h, ops, 24, cudaMemcpyDeviceToHost, st));
+  if (!dev) CK(cudaMemcpyAsync(y, a.y, nwin * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (static_cast<int>(h[2])) return fail(ctx, SCONV_ERR_FORMAT, "corrupted ptr value outside [-1, %d]", slot);
+  if (muls) *muls += h[0];
+  if (adds) *adds += h[1];
+  return SCONV_OK;
+}
+
+int sconv_cu_pecr_count(sconv_cu_ctx* ctx, const float* x, int c, int h, int w, int kh, int kw,
+                        int stride, int pool_w, int pool_h, int pool_stride, int32_t* count,
+                        int64_t* pack_start, int64_t* total, unsigned flags) {
+  if (!ctx) return fail(nullptr, SCONV_ERR_ARG, "null context");
+  if (c < 1) return fail(ctx, SCONV_ERR_SHAPE, "channels must be positive");
+  int OW, OH, PWo, PHo;
+  TRY(conv_dims(ctx, w, h, kw, kh, stride, &OW, &OH));
+  TRY(pack_count(ctx, w, kw, stride, pool_w, pool_stride, &PWo));
+  TRY(pack_count(ctx, h, kh, stride, pool_h, pool_stride, &PHo));
+  if (!x || !count || !pack_start || !total) return fail(ctx, SCONV_ERR_ARG, "null pointer");
+  const bool dev = flags & SCONV_F_DEVICE;
+  const int wpp = pool_w * pool_h, npacks = PHo * PWo;
+  DeviceGuard guard(ctx->device);
+  size_t scan_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, static_cast<int64_t*>(nullptr),
+                                static_cast<int64_t*>(nullptr), npacks);
+  Arena ar{ctx, {}};
+  const size_t ix = dev ? 0 : ar.add(size_t(c) * h * w * 4);
+  const size_t ic = dev ? 0 : ar.add(size_t(npacks) * wpp * 4);
+  const size_t is = dev ? 0 : ar.add(size_t(npacks + 1) * 8);
+  const size_t it = ar.add(size_t(npacks) * 8), iscan = ar.add(scan_bytes + 16);
+  std::vector<char*> p;
+  TRY(ar.commit(p));
+  cudaStream_t st = ctx->stream;
+  PecrFmtArgs a{x, c, h, w, kh, kw, stride, pool_w, pool_h, pool_stride, PHo, PWo, count,
+                nullptr, nullptr, nullptr};
+  int64_t* dstart = pack_start;
+  if (!dev) {
+    a.x = reinterpret_cast<float*>(p[ix]);
+    a.count = reinterpret_cast<int32_t*>(p[ic]);
+    dstart = reinterpret_cast<int64_t*>(p[is]);
+    CK(cudaMemcpyAsync(const_cast<float*>(a.x), x, size_t(c) * h * w * 4, cudaMemcpyHostToDevice, st));
+  }
+  pecr_export_kernel<0><<<grid_for(size_t(npacks) * wpp * 32, 256, 1 << 20), 256, 0, st>>>(a);
+  TRY(finish_launch(ctx, "pecr_export_kernel<count>"));
+  int64_t* tot = reinterpret_cast<int64_t*>(p[it]);
+  pecr_pack_totals_kernel<<<(npacks + 255) / 256, 256, 0, st>>>(a.count, wpp, npacks, tot);
+  TRY(finish_launch(ctx, "pecr_pack_totals_kernel"));
+  CK(cudaMemsetAsync(dstart, 0, 8, st));
+  CK(cub::DeviceScan::InclusiveSum(p[iscan], scan_bytes, tot, dstart + 1, npacks, st));
+  ctx->launches++;
+  int64_t htotal = 0;
+  CK(cudaMemcpyAsync(&htotal, dstart + npacks, 8, cudaMemcpyDeviceToHost, st));
+  if (!dev) {
+    CK(cudaMemcpyAsync(count, a.count, size_t(npacks) * wpp * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pack_start, dstart, size_t(npacks + 1) * 8, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  *total = htotal;
+  return SCONV_OK;
+}
+
+int sconv_cu_pecr_fill(sconv_cu_ctx* ctx, const float* x, int c, int h, int w, int kh, int kw,
+                       int stride, int pool_w, int pool_h, int pool_stride,
+                       const int64_t* pack_start, int64_t total, float* data, int32_t* index,
+                       unsigned flags) {
+  if (!ctx) return fail(nullptr, SCONV_ERR_ARG, "null context");
+  if (c < 1) return fail(ctx, SCONV_ERR_SHAPE, "channels must be positive");
+  int OW, OH, PWo, PHo;
+  TRY(conv_dims(ctx, w, h, kw, kh, stride, &OW, &OH));
+  TRY(pack_count(ctx, w, kw, stride, pool_w, pool_stride, &PWo));
+  TRY(pack_count(ctx, h, kh, stride, pool_h, pool_stride, &PHo));
+  if (!x || !pack_start || (total > 0 && (!data || !index)))
+    return fail(ctx, SCONV_ERR_ARG, "null pointer");
+  const bool dev = flags & SCONV_F_DEVICE;
+  const int wpp = pool_w * pool_h, npacks = PHo * PWo;
+  DeviceGuard guard(ctx->device);
+  // counts are recomputed on device (cheap) so the fill needs no host state
+  // beyond pack_start.
+  Arena ar{ctx, {}};
+  const size_t ix = dev ? 0 : ar.add(size_t(c) * h * w * 4);
+  const size_t is = dev ? 0 : ar.add(size_t(npacks + 1) * 8);
+  const size_t id = dev ? 0 : ar.add(size_t(std::max<int64_t>(total, 1)) * 4);
+  const size_t ii = dev ? 0 : ar.add(size_t(std::max<int64_t>(total, 1)) * 4);
+  const size_t ic = ar.add(size_t(npacks) * wpp * 4);
+  std::vector<char*> p;
+  TRY(ar.commit(p));
+  cudaStream_t st = ctx->stream;
+  PecrFmtArgs a{x, c, h, w, kh, kw, stride, pool_w, pool_h, pool_stride, PHo, PWo,
+                reinterpret_cast<int32_t*>(p[ic]), pack_start, data, index};
+  if (!dev) {
+    a.x = reinterpret_cast<float*>(p[ix]);
+    a.pack_start = reinterpret_cast<int64_t*>(p[is]);
+    a.data = reinterpret_cast<float*>(p[id]);
+    a.index = reinterpret_cast<int32_t*>(p[ii]);
+    CK(cudaMemcpyAsync(const_cast<float*>(a.x), x, size_t(c) * h * w * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(const_cast<int64_t*>(a.pack_start), pack_start, size_t(npacks + 1) * 8,
+                       cudaMemcpyHostToDevice, st));
+  }
+  const unsigned g = grid_for(size_t(npacks) * wpp * 32, 256, 1 << 20);
+  pecr_export_kernel<0><<<g, 256, 0, st>>>(a);
+  TRY(finish_launch(ctx, "pecr_export_kernel<count>"));
+  pecr_export_kernel<1><<<g, 256, 0, st>>>(a);
+  TRY(finish_launch(ctx, "pecr_export_kernel<fill>"));
+  if (!dev && total > 0) {
+    CK(cudaMemcpyAsync(data, a.data, size_t(total) * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(index, a.index, size_t(total) * 4, cudaMemcpyDeviceToHost, st));
+  }
+  if (!(flags & SCONV_F_ASYNC)) CK(cudaStreamSynchronize(st));
+  return SCONV_OK;
+}
+
+int sconv_cu_pecr_pool(sconv_cu_ctx* ctx, const int32_t* count, const int64_t* pack_start,
+                       const float* data, const int32_t* index, int64_t total,
+                       const float* kernel, int c, int kh, int kw, int packs_h, int packs_w,
+                       int pool_w, int pool_h, int mode, float* y, uint64_t* muls, uint64_t* adds,
+                       unsigned flags) {
+  if (!ctx) return fail(nullptr, SCONV_ERR_ARG, "null context");
+  if (c < 1 || kh < 1 || kw < 1 || packs_h < 1 || packs_w < 1 || pool_w < 1 || pool_h < 1)
+    return fail(ctx, SCONV_ERR_FORMAT, "bad PECR geometry");
+  if (mode != SCONV_POOL_MAX && mode != SCONV_POOL_MEAN)
+    return fail(ctx, SCONV_ERR_CONFIG, "unknown pool mode %d", mode);
+  if (!count || !pack_start || !kernel || !y || (total > 0 && (!data || !index)))
+    return fail(ctx, SCONV_ERR_ARG, "null pointer");
+  const bool dev = flags & SCONV_F_DEVICE, fast = flags & SCONV_F_FAST;
+  const int wpp = pool_w * pool_h, npacks = packs_h * packs_w, cap = c * kh * kw;
+  if (!dev) {  // check_pecr (src/pecr.cpp:40-55) on the host copy
+    for (int pk = 0; pk < npacks; ++pk) {
+      int64_t s = 0;
+      for (int q = 0; q < wpp; ++q) {
+        const int cn = count[size_t(pk) * wpp + q];
+        if (cn < 0 || cn > cap)
+          return fail(ctx, SCONV_ERR_FORMAT, "count entry %d outside [0, %d]", cn, cap);
+        s += cn;
+      }
+      if (pack_start[pk] < 0 || pack_start[pk + 1] - pack_start[pk] != s || pack_start[pk + 1] > total)
+        return fail(ctx, SCONV_ERR_FORMAT, "data/index length inconsistent with counts");
+    }
+    if (pack_start[npacks] != total)
+      return fail(ctx, SCONV_ERR_FORMAT, "data/index length inconsistent with counts");
+    for (int64_t q = 0; q < total; ++q)
+      if (index[q] < 0 || index[q] >= cap)
+        return fail(ctx, SCONV_ERR_FORMAT, "index entry %d out of range", index[q]);
+  }
+  DeviceGuard guard(ctx->device);
+  Arena ar{ctx, {}};
+  const size_t tb = size_t(std::max<int64_t>(total, 1)) * 4;
+  const size_t ic = dev ? 0 : ar.add(size_t(npacks) * wpp * 4), is = dev ? 0 : ar.add(size_t(npacks + 1) * 8);
+  const size_t id = dev ? 0 : ar.add(tb), ii = dev ? 0 : ar.add(tb);
+  const size_t ik = dev ? 0 : ar.add(size_t(cap) * 4), iy = dev ? 0 : ar.add(size_t(npacks) * 4);
+  const size_t iops = ar.add(64);
+  std::vector<char*> p;
+  TRY(ar.commit(p));
+  cudaStream_t st = ctx->stream;
+  auto* ops = reinterpret_cast<unsigned long long*>(p[iops]);
+  PecrPoolArgs a{count, pack_start, data, index, kernel, npacks, wpp, cap, mode, y, ops,
+                 reinterpret_cast<int*>(ops + 2)};
+  if (!dev) {
+    a.count = reinterpret_cast<int32_t*>(p[ic]);
+    a.pack_start = reinterpret_cast<int64_t*>(p[is]);
+    a.data = reinterpret_cast<float*>(p[id]);
+    a.index = reinterpret_cast<int32_t*>(p[ii]);
+    a.kernel = reinterpret_cast<float*>(p[ik]);
+    a.y = reinterpret_cast<float*>(p[iy]);
+    CK(cudaMemcpyAsync(const_cast<int32_t*>(a.count), count, size_t(npacks) * wpp * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(const_cast<int64_t*>(a.pack_start), pack_start, size_t(npacks + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (total > 0) {
+      CK(cudaMemcpyAsync(const_cast<float*>(a.data), data, size_t(total) * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(const_cast<int32_t*>(a.index), index, size_t(total) * 4, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemcpyAsync(const_cast<float*>(a.kernel), kernel, size_t(cap) * 4, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemsetAsync(ops, 0, 24, st));
+  if (dev) {
+    pecr_check_kernel<<<(npacks + 255) / 256, 256, 0, st>>>(a, total);
+    TRY(finish_launch(ctx, "pecr_check_kernel"));
+  }
+  if (fast) {
+    pecr_pool_fast_kernel<<<grid_for(size_t(npacks) * 32, 256, 1 << 20), 256, 0, st>>>(a);
+  } else {
+    pecr_pool_exact_kernel<<<grid_for(npacks, 256, 1 << 20), 256, 0, st>>>(a);
+  }
+  TRY(finish_launch(ctx, "pecr_pool_kernel"));
+  unsigned long long hh[3];
+  CK(cudaMemcpyAsync(hh, ops, 24, cudaMemcpyDeviceToHost, st));
+  if (!dev) CK(cudaMemcpyAsync(y, a.y, size_t(npacks) * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (static_cast<int>(hh[2])) return fail(ctx, SCONV_ERR_FORMAT, "corrupted PECR format");
+  if (muls) *muls += hh[0];
+  if (adds) *adds += hh[1];
+  return SCONV_OK;
+}
+
+int sconv_cu_ecr_conv_multi(sconv_cu_ctx** ctxs, int nctx, const float* x, int n, int c, int h,
+                            int w, const float* filters, int k, int kh, int kw, int stride,
+                            float* y, uint64_t* muls, uint64_t* adds, unsigned flags) {
+  if (flags & (SCONV_F_DEVICE | SCONV_F_ASYNC))
+    return fail(nullptr, SCONV_ERR_ARG, "multi-device entry takes host pointers");
+  int OW, OH;
+  TRY(conv_dims(nullptr, w, h, kw, kh, stride, &OW, &OH));
+  return run_multi(ctxs, nctx, n, k, size_t(c) * h * w, size_t(c) * kh * kw, size_t(OH) * OW, x,
+                   filters, y, muls, adds,
+                   [&](sconv_cu_ctx* cx, const float* xs, int ns, const float* ws, int ks,
+                       float* ys, uint64_t* m, uint64_t* a) {
+                     return sconv_cu_ecr_conv(cx, xs, ns, c, h, w, ws, ks, kh, kw, stride, ys, m,
+                                              a, flags);
+                   });
+}
+
+int sconv_cu_pecr_conv_pool_multi(sconv_cu_ctx** ctxs, int nctx, const float* x, int n, int c,
+                                  int h, int w, const float* filters, int k, int kh, int kw,
+                                  int stride, int pool_w, int pool_h, int pool_stride, int mode,
+                                  float* y, uint64_t* muls, uint64_t* adds, unsigned flags) {
+  if (flags & (SCONV_F_DEVICE | SCONV_F_ASYNC))
+    return fail(nullptr, SCONV_ERR_ARG, "multi-device entry takes host pointers");
+  int PWo, PHo;
+  TRY(pack_count(nullptr, w, kw, stride, pool_w, pool_stride, &PWo));
+  TRY(pack_count(nullptr, h, kh, stride, pool_h, pool_stride, &PHo));
+  return run_multi(ctxs, nctx, n, k, size_t(c) * h * w, size_t(c) * kh * kw, size_t(PHo) * PWo,
+                   x, filters, y, muls, adds,
+                   [&](sconv_cu_ctx* cx, const float* xs, int ns, const float* ws, int ks,
+                       float* ys, uint64_t* m, uint64_t* a) {
+                     return sconv_cu_pecr_conv_pool(cx, xs, ns, c, h, w, ws, ks, kh, kw, stride,
+                                                    pool_w, pool_h, pool_stride, mode, ys, m, a,
+                                                    flags);
+                   });
+}
+
+}  // extern "C"

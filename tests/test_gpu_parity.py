@@ -1,0 +1,323 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Checker: the C oracle (pinned to the reference by tests/test_oracle.py) and
+the golden vectors of the unmodified reference.  Bars:
+
+* index / count / format arrays: bit-exact;
+* EXACT arithmetic (default): outputs bit-exact;
+* FAST arithmetic (FFMA): |gpu - ref| <= ATOL + RTOL*|ref| with ATOL = RTOL
+  = 1e-5 (north_star: "within rel 1e-5 / abs 1e-5").
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ATOL = 1e-5
+RTOL = 1e-5
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def close(a, b):
+    return np.all(np.abs(a.astype(np.float64) - b) <= ATOL + RTOL * np.abs(b.astype(np.float64)))
+
+
+def inputs(orc, n, c, h, w, k, kh, kw, s, seed, mixed=True):
+    x = np.stack([orc.generate(h, w, c, s, seed + i) for i in range(n)])
+    f = np.stack([orc.generate(kh, kw, c, 0.0, seed + 1000 + j) for j in range(k)])
+    if mixed:
+        f = f - np.float32(0.5)
+    return x, f
+
+
+# ---------------------------------------------------------------------------
+# two-phase API: formats bit-exact
+# ---------------------------------------------------------------------------
+
+def test_fixture_f5(sc, golden):
+    fx = golden["fixtures"]
+    f5 = sc.FeatureMap(1, 5, 5, fx["f5"])
+    k3 = sc.Filter(1, 3, 3, fx["k3"])
+    e = sc.ecr_convert(f5, k3, sc.ConvConfig(1))
+    assert np.concatenate([r.ptr for r in e.block_rows]).tolist() == fx["ecr_ptr"]
+    assert np.concatenate([r.offsets for r in e.block_rows]).tolist() == fx["ecr_offsets"]
+    assert np.concatenate([r.f_data for r in e.block_rows]).tolist() == fx["ecr_f"]
+    assert np.concatenate([r.k_data for r in e.block_rows]).tolist() == fx["ecr_k"]
+    ops = sc.OpCount()
+    out = sc.ecr_spmv_conv(e, ops)
+    assert out.values.tolist() == fx["dense"] and (ops.multiplications, ops.additions) == (27, 18)
+    pool = sc.PoolConfig(2, 2, 1, sc.PoolMode.kMax)
+    p = sc.pecr_convert(f5, k3, sc.ConvConfig(1), pool)
+    assert np.concatenate([pk.count for row in p.pool_rows for pk in row]).tolist() == fx["pecr_count"]
+    assert np.concatenate([pk.data for row in p.pool_rows for pk in row]).tolist() == fx["pecr_data"]
+    assert np.concatenate([pk.index for row in p.pool_rows for pk in row]).tolist() == fx["pecr_index"]
+    pops = sc.OpCount()
+    pooled = sc.pecr_conv_pool(p, pops)
+    assert pooled.values.tolist() == [83, 75, 106, 106]
+    assert [pops.multiplications, pops.additions] == fx["pecr_ops"]
+    p.dims.pool.mode = sc.PoolMode.kMean
+    assert sc.pecr_conv_pool(p).values.tolist() == fx["pecr_mean"]
+    # the fused entries agree with the frozen values too
+    y = sc.pecr_conv_pool_batched(f5.array()[None], k3.array()[None], 1, pool)
+    assert y.reshape(-1).tolist() == [83, 75, 106, 106]
+    y = sc.ecr_conv_batched(f5.array()[None], k3.array()[None], 1)
+    assert y.reshape(-1).tolist() == fx["dense"]
+
+
+def test_golden_sweep_formats_and_outputs(sc, orc, golden):
+    for pt in golden["sweep"]:
+        x = orc.generate(pt["size"], pt["size"], pt["c"], pt["s"], pt["ms"])
+        w = orc.generate(pt["k"], pt["k"], pt["c"], 0.0, pt["ws"])
+        if pt["mixed"]:
+            w = w - np.float32(0.5)
+        m = sc.FeatureMap(pt["c"], pt["size"], pt["size"], x)
+        f = sc.Filter(pt["c"], pt["k"], pt["k"], w)
+        cfg = sc.ConvConfig(pt["stride"])
+        e = sc.ecr_convert(m, f, cfg)
+        cat = lambda key: np.concatenate([getattr(r, key) for r in e.block_rows])
+        assert orc.checksum(cat("ptr").view(np.float32)) == pt["ptr"]
+        assert orc.checksum(cat("offsets").view(np.float32)) == pt["offsets"]
+        assert orc.checksum(cat("f_data")) == pt["f_data"]
+        assert orc.checksum(cat("k_data")) == pt["k_data"]
+        ops = sc.OpCount()
+        y = sc.ecr_spmv_conv(e, ops)
+        assert orc.checksum(y.values) == pt["ecr"]
+        assert [ops.multiplications, ops.additions] == pt["ecr_ops"]
+        ops = sc.OpCount()
+        yb = sc.ecr_conv_batched(x[None], w[None], pt["stride"], counters=ops)
+        assert orc.checksum(yb) == pt["ecr"]
+        assert [ops.multiplications, ops.additions] == pt["ecr_ops"]
+        for ps in (1, 2):
+            g = pt.get(f"pecr_ps{ps}")
+            if g is None:
+                continue
+            pool = sc.PoolConfig(2, 2, ps, sc.PoolMode.kMax)
+            p = sc.pecr_convert(m, f, cfg, pool)
+            packs = [pk for row in p.pool_rows for pk in row]
+            assert orc.checksum(np.concatenate([pk.count for pk in packs]).view(np.float32)) == g["count"]
+            assert orc.checksum(np.concatenate([pk.data for pk in packs] + [np.zeros(0, np.float32)])) == g["data"]
+            assert orc.checksum(np.concatenate([pk.index for pk in packs] + [np.zeros(0, np.int32)]).view(np.float32)) == g["index"]
+            pops = sc.OpCount()
+            assert orc.checksum(sc.pecr_conv_pool(p, pops).values) == g["max"]
+            assert [pops.multiplications, pops.additions] == g["ops"]
+            pops = sc.OpCount()
+            yb = sc.pecr_conv_pool_batched(x[None], w[None], pt["stride"], pool, counters=pops)
+            assert orc.checksum(yb) == g["max"]
+            assert [pops.multiplications, pops.additions] == g["ops"]
+            mean = sc.PoolConfig(2, 2, ps, sc.PoolMode.kMean)
+            assert orc.checksum(sc.pecr_conv_pool_batched(x[None], w[None], pt["stride"], mean)) == g["mean"]
+
+
+def test_kats(sc, orc, golden):
+    for k in golden["kats"]:
+        x = orc.generate(k["h"], k["h"], k["c"], k["s"], k["ms"])
+        w = orc.generate(3, 3, k["c"], 0.0, k["ws"]) - np.float32(0.5)
+        assert sc.checksum_hex(sc.generate(k["h"], k["h"], k["c"], k["s"], k["ms"]).values) == k["map"]
+        ops = sc.OpCount()
+        y = sc.ecr_conv_batched(x[None], w[None], 1, counters=ops)
+        assert sc.checksum_hex(y) == k["ecr"]
+        assert [ops.multiplications, ops.additions] == k["ecr_ops"]
+        ops = sc.OpCount()
+        p = sc.pecr_conv_pool_batched(x[None], w[None], 1, sc.PoolConfig(2, 2, 2), counters=ops)
+        assert sc.checksum_hex(p) == k["pecr"]
+        assert [ops.multiplications, ops.additions] == k["pecr_ops"]
+
+
+# ---------------------------------------------------------------------------
+# fused batched path: tiled + generic kernels, EXACT bitwise, FAST tolerance
+# ---------------------------------------------------------------------------
+
+SHAPES = [
+    # n, c, h, w, k, kh, kw, stride, sparsity        (tiled: 3x3 s1, K >= 32)
+    (2, 3, 18, 20, 64, 3, 3, 1, 0.7),
+    (2, 13, 19, 23, 128, 3, 3, 1, 0.7),
+    (1, 64, 30, 30, 256, 3, 3, 1, 0.9),
+    (3, 17, 16, 34, 96, 3, 3, 1, 0.5),
+    (1, 8, 10, 10, 40, 3, 3, 1, 0.0),
+    (2, 9, 12, 12, 128, 3, 3, 1, 1.0),
+    (1, 5, 40, 9, 64, 3, 3, 1, 0.8),
+    # generic shapes
+    (2, 4, 11, 11, 7, 5, 5, 1, 0.7),
+    (2, 3, 17, 15, 5, 3, 3, 2, 0.5),
+    (1, 2, 12, 13, 3, 2, 2, 3, 0.6),
+    (1, 20, 11, 11, 50, 5, 5, 1, 0.7),   # LeNet conv2 shape
+    (2, 6, 9, 9, 33, 1, 1, 1, 0.7),
+    (1, 3, 8, 8, 16, 3, 3, 1, 0.7),     # K < 32 -> generic
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=[str(s) for s in SHAPES])
+def test_ecr_fused(sc, orc, shape):
+    n, c, h, w, k, kh, kw, s, sp = shape
+    x, f = inputs(orc, n, c, h, w, k, kh, kw, sp, seed=hash(shape) & 0xFFFF)
+    ref, rops = orc.ecr_conv(x, f, s)
+    for generic in (False, True):
+        ops = sc.OpCount()
+        y = sc.ecr_conv_batched(x, f, s, counters=ops, generic=generic)
+        assert bits_equal(y, ref), f"EXACT mismatch generic={generic}"
+        assert (ops.multiplications, ops.additions) == rops
+        yf = sc.ecr_conv_batched(x, f, s, fast=True, generic=generic)
+        assert close(yf, ref)
+    # empty windows produce +0.0 (ptr == -1 law)
+    nnz = np.stack([orc.window_nnz(x[i], kh, kw, s) for i in range(n)])
+    empty = np.broadcast_to(nnz[:, None] == 0, ref.shape)
+    assert not np.signbit(y[empty]).any() and not y[empty].any()
+
+
+PSHAPES = [
+    # n, c, h, w, k, kh, kw, stride, pw, ph, ps, sparsity
+    (2, 3, 18, 22, 64, 3, 3, 1, 2, 2, 2, 0.7),    # tiled P=2
+    (2, 19, 34, 34, 128, 3, 3, 1, 2, 2, 2, 0.7),
+    (1, 64, 16, 16, 256, 3, 3, 1, 2, 2, 2, 0.9),
+    (2, 5, 30, 14, 72, 3, 3, 1, 2, 2, 2, 0.5),
+    (2, 3, 9, 9, 5, 3, 3, 1, 2, 2, 1, 0.6),       # overlapping pool -> generic
+    (1, 4, 13, 13, 6, 3, 3, 2, 2, 2, 2, 0.7),
+    (1, 2, 13, 13, 4, 3, 3, 1, 3, 3, 2, 0.5),
+    (1, 3, 9, 9, 40, 3, 3, 1, 1, 1, 1, 0.7),
+]
+
+
+@pytest.mark.parametrize("shape", PSHAPES, ids=[str(s) for s in PSHAPES])
+def test_pecr_fused(sc, orc, shape):
+    n, c, h, w, k, kh, kw, s, pw, ph, ps, sp = shape
+    x, f = inputs(orc, n, c, h, w, k, kh, kw, sp, seed=hash(shape) & 0xFFFF)
+    for mode in (0, 1):
+        ref, rops = orc.pecr_conv(x, f, s, pw, ph, ps, mode)
+        pool = sc.PoolConfig(pw, ph, ps, sc.PoolMode(mode))
+        for generic in (False, True):
+            ops = sc.OpCount()
+            y = sc.pecr_conv_pool_batched(x, f, s, pool, counters=ops, generic=generic)
+            assert bits_equal(y, ref), f"EXACT mismatch mode={mode} generic={generic}"
+            assert (ops.multiplications, ops.additions) == rops
+            yf = sc.pecr_conv_pool_batched(x, f, s, pool, fast=True, generic=generic)
+            assert close(yf, ref)
+        # PECR == pool(relu(conv)) (test_pecr.cpp:35-42)
+        if mode == 0:
+            conv, _ = orc.ecr_conv(x, f, s)
+            sep = np.stack([orc.pool(orc.relu(conv[i]), pw, ph, ps, 0) for i in range(n)])
+            assert bits_equal(y, sep)
+
+
+def test_errors(sc):
+    x = np.ones((1, 2, 5, 5), np.float32)
+    with pytest.raises(sc.ShapeError):
+        sc.ecr_conv_batched(x, np.ones((3, 1, 3, 3), np.float32))
+    with pytest.raises(sc.ShapeError):
+        sc.ecr_conv_batched(np.ones((1, 1, 3, 3), np.float32), np.ones((1, 1, 5, 5), np.float32))
+    with pytest.raises(sc.ConfigError):
+        sc.ecr_conv_batched(x, np.ones((1, 2, 3, 3), np.float32), 0)
+    with pytest.raises(sc.ConfigError):  # 7x7, k3 -> 5 wide, pool 2 stride 2 dangles
+        sc.pecr_conv_pool_batched(np.ones((1, 1, 7, 7), np.float32),
+                                  np.ones((1, 1, 3, 3), np.float32), 1, sc.PoolConfig(2, 2, 2))
+    with pytest.raises(sc.ShapeError):
+        sc.ecr_convert(sc.FeatureMap(2, 5, 5), sc.Filter(1, 3, 3, np.ones(9)))
+
+
+def test_corrupted_formats(sc, orc):
+    """test_ecr.cpp:119-137, test_pecr.cpp:161-166."""
+    m = sc.FeatureMap(1, 5, 5, orc.generate(5, 5, 1, 0.5, 3))
+    f = sc.Filter(1, 3, 3, np.arange(1, 10))
+    e = sc.ecr_convert(m, f)
+    e.block_rows[1].ptr[1] = -2
+    with pytest.raises(sc.FormatError):
+        sc.ecr_spmv_conv(e)
+    e.block_rows[1].ptr[1] = 10
+    with pytest.raises(sc.FormatError):
+        sc.ecr_spmv_conv(e)
+    e = sc.ecr_convert(m, f)
+    e.block_rows.pop()
+    with pytest.raises(sc.FormatError):
+        sc.ecr_spmv_conv(e)
+    e = sc.ecr_convert(m, f)
+    e.block_rows[0].f_data = e.block_rows[0].f_data[:-1]
+    with pytest.raises(sc.FormatError):
+        sc.ecr_spmv_conv(e)
+    p = sc.pecr_convert(m, f, sc.ConvConfig(1), sc.PoolConfig(2, 2, 1))
+    p.pool_rows[0][0].data = np.append(p.pool_rows[0][0].data, np.float32(1))
+    with pytest.raises(sc.FormatError):
+        sc.pecr_conv_pool(p)
+    p = sc.pecr_convert(m, f, sc.ConvConfig(1), sc.PoolConfig(2, 2, 1))
+    if len(p.pool_rows[0][0].index):
+        p.pool_rows[0][0].index[0] = 99
+        with pytest.raises(sc.FormatError):
+            sc.pecr_conv_pool(p)
+
+
+def test_sentinel_law(sc):
+    """test_ecr.cpp:139-155: one nonzero -> one window with ptr 1, rest -1 / +0.0."""
+    m = sc.FeatureMap(1, 6, 6)
+    m.values[0] = 2.5
+    f = sc.Filter(1, 3, 3, np.arange(1, 10))
+    e = sc.ecr_convert(m, f)
+    ptr = np.stack([r.ptr for r in e.block_rows])
+    expect = -np.ones((4, 4), np.int32)
+    expect[0, 0] = 1
+    assert np.array_equal(ptr, expect)
+    out = sc.ecr_spmv_conv(e).array()[0]
+    assert out[0, 0] == 2.5 and not np.signbit(out).any() and (out[1:] == 0).all()
+
+
+def test_all_zero_map(sc):
+    """acceptance criterion 9 (acceptance_main.cpp:426-475)."""
+    x = np.zeros((2, 3, 16, 16), np.float32)
+    w = np.random.default_rng(0).random((64, 3, 3, 3), np.float32) - 0.5
+    for fn, args in ((sc.ecr_conv_batched, ()), (sc.pecr_conv_pool_batched, (sc.PoolConfig(2, 2, 2),))):
+        ops = sc.OpCount()
+        y = fn(x, w, 1, *args, counters=ops)
+        assert not y.any() and not np.signbit(y).any()
+        assert ops.multiplications == 0 and ops.additions == 0
+    e = sc.ecr_convert(sc.FeatureMap(3, 16, 16), sc.Filter(3, 3, 3, w[0]))
+    assert all((r.ptr == -1).all() for r in e.block_rows)
+
+
+def test_windows_reconstruct(sc, orc):
+    """Lossless windows (test_ecr.cpp:198-206, test_pecr.cpp:219-229)."""
+    x = orc.generate(13, 13, 3, 0.7, 11)
+    m = sc.FeatureMap(3, 13, 13, x)
+    f = sc.Filter(3, 3, 3, orc.generate(3, 3, 3, 0.0, 12))
+    e = sc.ecr_convert(m, f, sc.ConvConfig(2))
+    for b in range(e.dims.out_h()):
+        for t in range(e.dims.out_w()):
+            assert np.array_equal(sc.ecr_window(e, b, t), x[:, 2 * b:2 * b + 3, 2 * t:2 * t + 3].reshape(-1))
+    p = sc.pecr_convert(m, f, sc.ConvConfig(1), sc.PoolConfig(2, 2, 1))
+    for b in range(p.packs_h()):
+        for t in range(p.packs_w()):
+            for n in range(4):
+                wy, wx = b + n // 2, t + n % 2
+                assert np.array_equal(sc.pecr_window(p, b, t, n), x[:, wy:wy + 3, wx:wx + 3].reshape(-1))
+
+
+def test_multichannel_conv(sc, orc):
+    x = orc.generate(12, 12, 4, 0.6, 5)
+    fs = [sc.Filter(4, 3, 3, orc.generate(3, 3, 4, 0.0, 100 + i) - np.float32(0.5)) for i in range(40)]
+    out = sc.multichannel_conv(sc.FeatureMap(4, 12, 12, x), fs, sc.ConvConfig(1))
+    ref, _ = orc.ecr_conv(x[None], np.stack([f.array() for f in fs]), 1)
+    assert bits_equal(out.array(), ref[0])
+
+
+def test_torch_device_path(sc, orc):
+    torch = pytest.importorskip("torch")
+    x, f = inputs(orc, 2, 16, 20, 20, 128, 3, 3, 0.7, seed=77)
+    ref, _ = orc.ecr_conv(x, f, 1)
+    xd, fd = torch.from_numpy(x).cuda(), torch.from_numpy(f).cuda()
+    y = sc.ecr_conv_batched(xd, fd, 1)
+    torch.cuda.synchronize()
+    assert bits_equal(y.cpu().numpy(), ref)
+    y2 = sc.ecr_conv_batched(xd, fd, 1, sync=False)
+    torch.cuda.synchronize()
+    assert bits_equal(y2.cpu().numpy(), ref)
+    p = sc.pecr_conv_pool_batched(xd, fd, 1, sc.PoolConfig(2, 2, 2))
+    pref, _ = orc.pecr_conv(x, f, 1, 2, 2, 2, 0)
+    assert bits_equal(p.cpu().numpy(), pref)
+
+
+def test_determinism(sc, orc):
+    x, f = inputs(orc, 2, 32, 30, 30, 128, 3, 3, 0.7, seed=3)
+    a = sc.ecr_conv_batched(x, f, 1, fast=True)
+    for _ in range(3):
+        assert bits_equal(sc.ecr_conv_batched(x, f, 1, fast=True), a)

@@ -1,0 +1,148 @@
+"""Host-side checks that need no GPU: the C-ABI library loads and exports
+every entry point include/sconv_cuda.h declares; host geometry, partition,
+generator and checksum agree with the reference; the product never reaches
+into oracle/."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+HEADER = os.path.join(ROOT, "include", "sconv_cuda.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sconv_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(sc):
+    lib = sc._native.lib()
+    decl = declared_symbols()
+    assert len(decl) >= 25
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert set(decl) == set(sc._native.SYMBOLS)
+    out = subprocess.run(["nm", "-D", "--defined-only", sc.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (sconv_\w+)", out))
+    assert set(decl) <= exported
+
+
+def test_library_is_sm100a(sc):
+    out = subprocess.run(["cuobjdump", "--list-elf", sc.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_no_device(sc):
+    assert b"sm_100a" in sc._native.lib().sconv_cu_version()
+
+
+def test_geometry_errors(sc, golden):
+    assert sc.conv_output_dims(5, 5, 3, 3, 1) == sc.OutputDims(3, 3)
+    assert sc.conv_output_dims(11, 11, 3, 3, 2) == sc.OutputDims(5, 5)
+    assert sc.ecr_grid_shape(5, 5, 5, 5, 1) == sc.EcrGridShape(1, 1)
+    with pytest.raises(sc.ShapeError):
+        sc.conv_output_dims(3, 3, 5, 5, 1)
+    with pytest.raises(sc.ConfigError):
+        sc.conv_output_dims(5, 5, 3, 3, 0)
+    for case in golden["pack_count"]:
+        if "packs" in case:
+            assert sc.pecr_pack_count(*case["args"]) == case["packs"]
+        else:
+            with pytest.raises(getattr(sc, case["error"])):
+                sc.pecr_pack_count(*case["args"])
+
+
+def test_pack_count_matches_enumeration(sc):
+    """test_pecr.cpp:61-83: accepted tilings equal brute-force enumeration."""
+    def windows(i, k, s):
+        return len(range(0, i - k + 1, s)) if k <= i else 0
+    for i in range(5, 25):
+        for k in (2, 3, 5):
+            for cs in (1, 2):
+                for pw in (1, 2, 3):
+                    for ps in (1, 2):
+                        if k > i:
+                            continue
+                        try:
+                            packs = sc.pecr_pack_count(i, k, cs, pw, ps)
+                        except sc.ConfigError:
+                            continue
+                        assert packs == windows(windows(i, k, cs), pw, ps)
+
+
+def test_generate_bit_identical(sc, golden, orc):
+    for g in golden["generate"]:
+        m = sc.generate(g["h"], g["w"], g["c"], g["s"], g["seed"])
+        assert sc.checksum_hex(m.values) == g["checksum"]
+    seeds = [5, 6, 7, 8, 9]
+    b = sc.generate_batch(seeds, 20, 17, 3, 0.7, threads=3)
+    for i, s in enumerate(seeds):
+        assert np.array_equal(b[i], orc.generate(20, 17, 3, 0.7, s))
+    with pytest.raises(sc.ConfigError):
+        sc.generate(4, 4, 1, 1.5, 0)
+    with pytest.raises(sc.ShapeError):
+        sc.generate(0, 4, 1, 0.5, 0)
+
+
+def test_checksum(sc, orc):
+    assert sc.checksum_hex(np.zeros(0, np.float32)) == "cbf29ce484222325"  # test_report.cpp:10
+    v = np.array([0.0, -0.0, 1.5, np.inf], np.float32)
+    assert sc.checksum_hex(v) == orc.checksum(v)
+    assert sc.checksum_hex(np.array([0.0], np.float32)) != sc.checksum_hex(np.array([-0.0], np.float32))
+
+
+def test_shard_partition(sc):
+    for n, k, world in [(64, 512, 8), (512, 64, 8), (3, 512, 8), (7, 5, 3), (1, 1, 1), (0, 64, 2)]:
+        cover = np.zeros((n, k), np.int32)
+        for r in range(world):
+            n0, n1, k0, k1 = sc.shard(n, k, world, r)
+            cover[n0:n1, k0:k1] += 1
+        assert (cover == 1).all()
+    with pytest.raises(sc.ConfigError):
+        sc.shard(4, 4, 2, 2)
+
+
+def test_launch_plan(sc):
+    p = sc.launch_plan(64, 256, 58, 58, 256, 3, 3, 1)
+    assert p["kernel"] == 1 and p["grid_z"] == 64 and p["grid_y"] == 2 and p["block_threads"] == 128
+    p = sc.launch_plan(64, 64, 226, 226, 64, 3, 3, 1, sc.PoolConfig(2, 2, 2))
+    assert p["kernel"] == 2 and p["smem_bytes"] <= 227 * 1024
+    assert sc.launch_plan(1, 20, 11, 11, 50, 5, 5, 1)["kernel"] == 0
+
+
+def test_value_types(sc):
+    with pytest.raises(sc.ShapeError):
+        sc.FeatureMap(1, 2, 2, np.zeros(3))
+    with pytest.raises(sc.ShapeError):
+        sc.Filter(0, 3, 3, np.zeros(0))
+    ops = sc.OpCount(1, 2)
+    ops.merge(sc.OpCount(3, 4))
+    assert ops == sc.OpCount(4, 6)
+    d = sc.PecrDims(9, 9, 3, 3, 2, 1, sc.PoolConfig(2, 2, 1))
+    assert d.tile_w() == 5 and d.tile_h() == 5 and d.capacity() == 36
+
+
+def test_no_device_fails_loudly(sc):
+    """No silent CPU fallback: without a GPU the compute entries raise."""
+    import ctypes
+    n = ctypes.c_int(0)
+    sc._native.lib().sconv_cu_device_count(ctypes.byref(n))
+    if n.value > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(sc.CudaError):
+        sc.ecr_conv_batched(np.ones((1, 1, 5, 5), np.float32), np.ones((1, 1, 3, 3), np.float32))
+
+
+def test_product_does_not_touch_oracle():
+    pkg = os.path.join(ROOT, "paper_1909_09927_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h", ".hpp")) and "dropin" not in dirpath:
+                text = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", text).replace("oracle/_ref", ""), f
