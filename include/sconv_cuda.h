@@ -71,9 +71,12 @@ const char* sconv_cu_version(void);
 int sconv_cu_device_count(int* count);
 int sconv_cu_ctx_create(int device, sconv_cu_ctx** out);
 int sconv_cu_ctx_destroy(sconv_cu_ctx* ctx);
-/* Run on an external cudaStream_t (e.g. torch's current stream); NULL
- * restores the context's own stream. */
+/* Run on an external cudaStream_t (e.g. torch's current stream).  The value
+ * is used as is: NULL is the legacy default stream.  Both calls drain the
+ * previous stream first (the context workspace is stream-ordered). */
 int sconv_cu_ctx_set_stream(sconv_cu_ctx* ctx, void* stream);
+/* Go back to the context's own non-blocking stream. */
+int sconv_cu_ctx_use_own_stream(sconv_cu_ctx* ctx);
 void* sconv_cu_ctx_stream(sconv_cu_ctx* ctx);
 int sconv_cu_ctx_device(sconv_cu_ctx* ctx);
 int sconv_cu_synchronize(sconv_cu_ctx* ctx);

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libsconv_cuda.so")
 # exported symbols (kept in sync with include/sconv_cuda.h; tests check both)
 SYMBOLS = (
     "sconv_cu_version", "sconv_cu_device_count", "sconv_cu_ctx_create", "sconv_cu_ctx_destroy",
-    "sconv_cu_ctx_set_stream", "sconv_cu_ctx_stream", "sconv_cu_ctx_device",
+    "sconv_cu_ctx_set_stream", "sconv_cu_ctx_use_own_stream", "sconv_cu_ctx_stream", "sconv_cu_ctx_device",
     "sconv_cu_synchronize", "sconv_cu_last_error", "sconv_cu_launch_count",
     "sconv_conv_output_dims", "sconv_pecr_pack_count", "sconv_cu_plan", "sconv_cu_ecr_conv",
     "sconv_cu_pecr_conv_pool", "sconv_cu_ecr_convert", "sconv_cu_ecr_spmv", "sconv_cu_pecr_count",
@@ -59,6 +59,7 @@ def lib() -> C.CDLL:
     L.sconv_cu_ctx_create.argtypes = [_i, C.POINTER(_vp)]
     L.sconv_cu_ctx_destroy.argtypes = [_vp]
     L.sconv_cu_ctx_set_stream.argtypes = [_vp, _vp]
+    L.sconv_cu_ctx_use_own_stream.argtypes = [_vp]
     L.sconv_cu_ctx_stream.argtypes = [_vp]
     L.sconv_cu_ctx_stream.restype = _vp
     L.sconv_cu_ctx_device.argtypes = [_vp]
@@ -109,12 +110,18 @@ class Context:
         check(lib().sconv_cu_ctx_create(device, C.byref(h)))
         self.handle = h
         self.device = device
-        self._stream = None
+        self._stream = "own"
 
-    def set_stream(self, stream_ptr: int | None) -> None:
+    def set_stream(self, stream_ptr: int) -> None:
+        """Use an external cudaStream_t (0 = legacy default stream)."""
         if stream_ptr != self._stream:
             check(lib().sconv_cu_ctx_set_stream(self.handle, stream_ptr), self.handle)
             self._stream = stream_ptr
+
+    def use_own_stream(self) -> None:
+        if self._stream != "own":
+            check(lib().sconv_cu_ctx_use_own_stream(self.handle), self.handle)
+            self._stream = "own"
 
     def synchronize(self) -> None:
         check(lib().sconv_cu_synchronize(self.handle), self.handle)

@@ -521,6 +521,7 @@ def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, co
         if out is None:
             out = np.empty(shape, np.float32)
         ctx = nat.context(0 if device is None else device)
+        ctx.use_own_stream()
         xp, wp, yp = _ptr(x), _ptr(filters), _ptr(out)
     m, a = C.c_uint64(0), C.c_uint64(0)
     mp = C.byref(m) if counters is not None else None

@@ -71,30 +71,48 @@ struct TiledArgs {
   int mode;         // pool mode (P > 0)
 };
 
+// Lane <-> channel map.  Lane l of a warp owns R output channels; for R >= 4
+// they are {g*128 + 4l + q : g < R/4, q < 4} so each group of four is one
+// conflict-free LDS.128 of a 512-byte weight row; for R < 4 they are
+// {R*l + q}.
 template <int R>
-__device__ __forceinline__ void lds_r(float (&dst)[R], const float* src) {
-  if constexpr (R == 8) {
-    const float4 a = *reinterpret_cast<const float4*>(src);
-    const float4 b = *reinterpret_cast<const float4*>(src + 4);
-    dst[0] = a.x; dst[1] = a.y; dst[2] = a.z; dst[3] = a.w;
-    dst[4] = b.x; dst[5] = b.y; dst[6] = b.z; dst[7] = b.w;
-  } else if constexpr (R == 4) {
-    const float4 a = *reinterpret_cast<const float4*>(src);
-    dst[0] = a.x; dst[1] = a.y; dst[2] = a.z; dst[3] = a.w;
-  } else if constexpr (R == 2) {
-    const float2 a = *reinterpret_cast<const float2*>(src);
-    dst[0] = a.x; dst[1] = a.y;
+__device__ __forceinline__ int lane_chan(int lane, int r) {
+  if constexpr (R >= 4) {
+    return (r / 4) * 128 + lane * 4 + (r % 4);
   } else {
-    dst[0] = src[0];
+    return lane * R + r;
   }
 }
 
-template <class Cfg, bool FAST, int MINB>
+template <int R>
+__device__ __forceinline__ void lds_w(float (&dst)[R], const float* row, int lane) {
+  if constexpr (R >= 4) {
+#pragma unroll
+    for (int g = 0; g < R / 4; ++g) {
+      const float4 a = *reinterpret_cast<const float4*>(row + g * 128 + lane * 4);
+      dst[4 * g + 0] = a.x;
+      dst[4 * g + 1] = a.y;
+      dst[4 * g + 2] = a.z;
+      dst[4 * g + 3] = a.w;
+    }
+  } else if constexpr (R == 2) {
+    const float2 a = *reinterpret_cast<const float2*>(row + lane * 2);
+    dst[0] = a.x;
+    dst[1] = a.y;
+  } else {
+    dst[0] = row[lane];
+  }
+}
+
+// NOSKIP (calibration only) multiplies zeros too: identical results, dense work.
+template <class Cfg, bool FAST, int MINB, bool NOSKIP = false>
 __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArgs a) {
   constexpr int KH = Cfg::KH, KW = Cfg::KW, S = Cfg::S, TH = Cfg::TH, TW = Cfg::TW, R = Cfg::R;
   constexpr int KK = Cfg::KK, KT = Cfg::KT, CC = Cfg::CC, P = Cfg::P;
   constexpr int PH = Cfg::PH, PW = Cfg::PW, PWS = Cfg::PWS;
   constexpr int WPH = Cfg::WPH, WPW = Cfg::WPW, WPW4 = Cfg::WPW4;
+  constexpr int NPOS = WPH * WPW;  // input positions a warp visits per channel
+  static_assert(NPOS <= 64, "warp patch must fit two ballots");
 
   extern __shared__ float4 smem_raw[];
   float* smem = reinterpret_cast<float*>(smem_raw);
@@ -114,34 +132,59 @@ __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArg
   const float* xn = a.x + static_cast<size_t>(n) * C * H * W;
 
   // ---- cp.async staging of one CC-channel chunk -------------------------
+  // Input patch: thread t owns patch elements t, t+NT, ... (fixed across
+  // chunks), so the per-copy work is one address increment of H*W.
+  constexpr int PE = PH * PW;
+  constexpr int EPT = (PE + Cfg::NT - 1) / Cfg::NT;  // patch elements per thread
+  const size_t plane = static_cast<size_t>(H) * W;
+  const float* in_src[EPT];
+  int in_dst[EPT];
+  bool in_ok[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int idx = tid + e * Cfg::NT;
+    const int yy = idx / PW, xx = idx - (idx / PW) * PW;
+    const int gy = iy0 + yy, gx = ix0 + xx;
+    in_ok[e] = idx < PE && gy < H && gx < W;
+    in_src[e] = in_ok[e] ? xn + static_cast<size_t>(gy) * W + gx : xn;
+    in_dst[e] = yy * PWS + xx;
+  }
+  // Weights: rows (c, ij) of KT floats, contiguous per row in wt.
+  constexpr int QW = KT / 4;                 // float4 per weight row
+  constexpr int RSTEP = Cfg::NT / QW;        // rows covered per pass
+  static_assert(Cfg::NT % QW == 0, "thread count must cover whole weight rows");
+  const int wq = tid % QW, wrow0 = tid / QW;
+  const bool wk_ok = k0 + 4 * wq < K;
+
   auto stage = [&](int c0, int buf) {
     float* in_s = smem + buf * Cfg::STAGE;
     float* w_s = in_s + Cfg::IN_STAGE;
-    for (int idx = tid; idx < CC * PH * PW; idx += Cfg::NT) {
-      const int c = idx / (PH * PW);
-      const int rem = idx - c * (PH * PW);
-      const int yy = rem / PW, xx = rem - (rem / PW) * PW;
-      const int gc = c0 + c, gy = iy0 + yy, gx = ix0 + xx;
-      const bool ok = gc < C && gy < H && gx < W;
-      const float* src = ok ? xn + (static_cast<size_t>(gc) * H + gy) * W + gx : xn;
-      cp_async4(in_s + (c * PH + yy) * PWS + xx, src, ok);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      if (tid + e * Cfg::NT < PE) {
+        const float* src = in_src[e] + c0 * plane;
+        float* dst = in_s + in_dst[e];
+#pragma unroll
+        for (int c = 0; c < CC; ++c) {
+          const bool ok = in_ok[e] && c0 + c < C;
+          cp_async4(dst + c * PH * PWS, ok ? src + c * plane : xn, ok);
+        }
+      }
     }
+    const int rows_left = (C - c0) * KK;  // valid weight rows from c0
     if ((K & 3) == 0) {
-      for (int idx = tid; idx < CC * KK * (KT / 4); idx += Cfg::NT) {
-        const int row = idx / (KT / 4), q = idx - row * (KT / 4);
-        const int c = row / KK, ij = row - c * KK;
-        const int gc = c0 + c, k = k0 + 4 * q;
-        const bool ok = gc < C && k < K;
-        const float* src = ok ? a.wt + (static_cast<size_t>(gc) * KK + ij) * K + k : a.wt;
-        cp_async16(w_s + row * KT + 4 * q, src, ok);
+      const float* wsrc = a.wt + static_cast<size_t>(c0) * KK * K + k0 + 4 * wq;
+      float* wdst = w_s + 4 * wq;
+#pragma unroll 4
+      for (int row = wrow0; row < CC * KK; row += RSTEP) {
+        const bool ok = wk_ok && row < rows_left;
+        cp_async16(wdst + row * KT, ok ? wsrc + static_cast<size_t>(row) * K : a.wt, ok);
       }
     } else {
       for (int idx = tid; idx < CC * KK * KT; idx += Cfg::NT) {
         const int row = idx / KT, q = idx - row * KT;
-        const int c = row / KK, ij = row - c * KK;
-        const int gc = c0 + c, k = k0 + q;
-        const bool ok = gc < C && k < K;
-        const float* src = ok ? a.wt + (static_cast<size_t>(gc) * KK + ij) * K + k : a.wt;
+        const bool ok = row < rows_left && k0 + q < K;
+        const float* src = ok ? a.wt + (static_cast<size_t>(c0) * KK + row) * K + k0 + q : a.wt;
         cp_async4(w_s + row * KT + q, src, ok);
       }
     }
@@ -155,6 +198,13 @@ __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArg
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[i][j][r] = 0.0f;
 
+  // Lane l tests positions l and l+32 of the warp patch; the two ballots are
+  // the ECR nonzero index of this (channel, patch), uniform across the warp.
+  const int wbase = (wsy * TH * S) * PWS + wsx * TW * S;
+  const int q0 = lane, q1 = lane + 32;
+  const int off0 = wbase + (q0 / WPW) * PWS + q0 % WPW;
+  const int off1 = q1 < NPOS ? wbase + (q1 / WPW) * PWS + q1 % WPW : wbase;
+
   const int nchunks = (C + CC - 1) / CC;
   stage(0, 0);
   cp_async_commit();
@@ -167,14 +217,18 @@ __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArg
     const float* in_s = smem + (ch & 1) * Cfg::STAGE;
     const float* w_s = in_s + Cfg::IN_STAGE;
     const int cn = min(CC, C - ch * CC);
+    const float* ic = in_s;
+    const float* wsrc = w_s + wk * 32 * R;
 #pragma unroll 1
-    for (int c = 0; c < cn; ++c) {
-      float wr[KK][R];
-      const float* wsrc = w_s + c * KK * KT + wk * 32 * R + lane * R;
-#pragma unroll
-      for (int ij = 0; ij < KK; ++ij) lds_r<R>(wr[ij], wsrc + ij * KT);
+    for (int c = 0; c < cn; ++c, ic += PH * PWS, wsrc += KK * KT) {
+      const unsigned m0 = __ballot_sync(kFull, ic[off0] != 0.0f);
+      const unsigned m1 = NPOS > 32 ? __ballot_sync(kFull, q1 < NPOS && ic[off1] != 0.0f) : 0u;
 
-      const float* is = in_s + c * PH * PWS + (wsy * TH * S) * PWS + wsx * TW * S;
+      float wr[KK][R];
+#pragma unroll
+      for (int ij = 0; ij < KK; ++ij) lds_w<R>(wr[ij], wsrc + ij * KT, lane);
+
+      const float* is = ic + wbase;
 #pragma unroll
       for (int Y = 0; Y < WPH; ++Y) {
         float row[WPW4];
@@ -188,8 +242,10 @@ __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArg
         }
 #pragma unroll
         for (int X = 0; X < WPW; ++X) {
-          const float v = row[X];
-          if (v != 0.0f) {  // warp-uniform: every lane holds the same v
+          const int p = Y * WPW + X;
+          const bool nz = p < 32 ? ((m0 >> p) & 1u) : ((m1 >> (p - 32)) & 1u);
+          if (NOSKIP || nz) {  // uniform: the mask came from a ballot
+            const float v = row[X];
 #pragma unroll
             for (int i = 0; i < KH; ++i) {
               const int dy = Y - i;
@@ -211,7 +267,7 @@ __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArg
   }
 
   // ---- epilogue ----------------------------------------------------------
-  const int kl = k0 + wk * 32 * R + lane * R;
+  const int kw0 = k0 + wk * 32 * R;
   if constexpr (P == 0) {
     const int gx0 = ox0 + wsx * TW;
     const bool vec = (a.OW % 4 == 0) && (TW % 4 == 0);
@@ -221,7 +277,7 @@ __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArg
       if (gy >= a.OH) continue;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int k = kl + r;
+        const int k = kw0 + lane_chan<R>(lane, r);
         if (k >= K) continue;
         float* dst = a.y + ((static_cast<size_t>(n) * K + k) * a.OH + gy) * a.OW + gx0;
         if (vec) {
@@ -248,7 +304,7 @@ __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArg
       if (py0 + py >= PHo) continue;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int k = kl + r;
+        const int k = kw0 + lane_chan<R>(lane, r);
         if (k >= K) continue;
         float* dst = a.y + ((static_cast<size_t>(n) * K + k) * PHo + py0 + py) * PWo + px0;
 #pragma unroll

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -149,14 +150,25 @@ int finish_launch(sconv_cu_ctx* ctx, const char* what) {
 // Tiled kernel registry.  Specialisations exist for the VGG / AlexNet /
 // GoogLeNet 3x3 stride-1 shapes; every other shape takes the generic kernel.
 // ---------------------------------------------------------------------------
-template <int P>
-using Cfg3x3R4 = TiledCfg<3, 3, 1, 4, 8, 4, 1, 2, 2, 8, P>;  // 8x16 outputs x 128 channels
-template <int P>
-using Cfg3x3R2 = TiledCfg<3, 3, 1, 4, 8, 2, 1, 2, 2, 8, P>;  // 8x16 outputs x 64 channels
+// TiledCfg<KH, KW, S, TH, TW, R, WK, WSY, WSX, CC, P> -- warp tile TH x TW
+// outputs x 32R channels, CTA = WSY x WSX warps (x WK along channels).
+template <int P> using Cfg1 = TiledCfg<3, 3, 1, 4, 4, 8, 1, 2, 4, 8, P>;  // 8x16 x 256ch
+template <int P> using Cfg2 = TiledCfg<3, 3, 1, 4, 4, 4, 1, 2, 4, 8, P>;  // 8x16 x 128ch
+template <int P> using Cfg3 = TiledCfg<3, 3, 1, 4, 8, 4, 1, 2, 2, 8, P>;  // 8x16 x 128ch
+template <int P> using Cfg4 = TiledCfg<3, 3, 1, 4, 8, 2, 1, 2, 2, 8, P>;  // 8x16 x 64ch
+template <int P> using Cfg5 = TiledCfg<3, 3, 1, 2, 8, 8, 1, 4, 2, 8, P>;  // 8x16 x 256ch
+template <int P> using Cfg6 = TiledCfg<3, 3, 1, 4, 4, 2, 1, 2, 4, 8, P>;  // 8x16 x 64ch
+template <int P> using Cfg7 = TiledCfg<3, 3, 1, 2, 4, 4, 1, 4, 2, 8, P>;  // 8x8 x 128ch
+constexpr int kNumCfgs = 7;
 
-template <class Cfg, bool FAST>
+template <class Cfg>
+constexpr int min_blocks() {
+  return Cfg::R >= 8 ? 1 : 2;
+}
+
+template <class Cfg, bool FAST, bool NOSKIP = false>
 int launch_tiled_cfg(sconv_cu_ctx* ctx, const TiledArgs& a, int N) {
-  auto kern = ecr_tiled_kernel<Cfg, FAST, 2>;
+  auto kern = ecr_tiled_kernel<Cfg, FAST, min_blocks<Cfg>(), NOSKIP>;
   static bool attr_done[64] = {};
   const int slot = ctx->device & 63;
   if (!attr_done[slot]) {
@@ -172,19 +184,43 @@ int launch_tiled_cfg(sconv_cu_ctx* ctx, const TiledArgs& a, int N) {
   return finish_launch(ctx, "ecr_tiled_kernel");
 }
 
+int forced_cfg() {
+  static const int v = [] {
+    const char* e = std::getenv("SCONV_TILED_CFG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 // which tiled config (0 = none -> generic)
 int pick_tiled(int K, int kh, int kw, int S, int P) {
-  if (kh == 3 && kw == 3 && S == 1 && (P == 0 || P == 2) && K >= 32) return K % 128 == 0 ? 1 : 2;
-  return 0;
+  if (!(kh == 3 && kw == 3 && S == 1 && (P == 0 || P == 2) && K >= 32)) return 0;
+  const int f = forced_cfg();
+  if ((f >= 1 && f <= kNumCfgs) || (f >= 11 && f <= 17 && P == 0)) return f;
+  if (K % 128 == 0) return 2;  // measured best on VGG K=128..512 (tools/tune.py)
+  return 4;
+}
+
+template <template <int> class CfgT, bool FAST>
+int launch_p(sconv_cu_ctx* ctx, int P, const TiledArgs& a, int N) {
+  return P == 0 ? launch_tiled_cfg<CfgT<0>, FAST>(ctx, a, N)
+                : launch_tiled_cfg<CfgT<2>, FAST>(ctx, a, N);
 }
 
 template <bool FAST>
 int launch_tiled(sconv_cu_ctx* ctx, int which, int P, const TiledArgs& a, int N) {
-  if (which == 1)
-    return P == 0 ? launch_tiled_cfg<Cfg3x3R4<0>, FAST>(ctx, a, N)
-                  : launch_tiled_cfg<Cfg3x3R4<2>, FAST>(ctx, a, N);
-  return P == 0 ? launch_tiled_cfg<Cfg3x3R2<0>, FAST>(ctx, a, N)
-                : launch_tiled_cfg<Cfg3x3R2<2>, FAST>(ctx, a, N);
+  switch (which) {
+    case 1: return launch_p<Cfg1, FAST>(ctx, P, a, N);
+    case 2: return launch_p<Cfg2, FAST>(ctx, P, a, N);
+    case 3: return launch_p<Cfg3, FAST>(ctx, P, a, N);
+    case 4: return launch_p<Cfg4, FAST>(ctx, P, a, N);
+    case 5: return launch_p<Cfg5, FAST>(ctx, P, a, N);
+    case 6: return launch_p<Cfg6, FAST>(ctx, P, a, N);
+    case 17: return launch_tiled_cfg<Cfg7<0>, FAST, true>(ctx, a, N);  // calibration
+    case 11: return launch_tiled_cfg<Cfg1<0>, FAST, true>(ctx, a, N);  // calibration
+    case 12: return launch_tiled_cfg<Cfg2<0>, FAST, true>(ctx, a, N);  // calibration
+    default: return launch_p<Cfg7, FAST>(ctx, P, a, N);
+  }
 }
 
 template <class Cfg>
@@ -198,6 +234,21 @@ void fill_plan(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
   p->tile_h = Cfg::OTH;
   p->tile_w = Cfg::OTW;
   p->tile_k = Cfg::KT;
+}
+
+void plan_for(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
+  switch (which) {
+    case 1: return fill_plan<Cfg1<0>>(p, which, N, K, OH, OW);
+    case 2: return fill_plan<Cfg2<0>>(p, which, N, K, OH, OW);
+    case 3: return fill_plan<Cfg3<0>>(p, which, N, K, OH, OW);
+    case 4: return fill_plan<Cfg4<0>>(p, which, N, K, OH, OW);
+    case 5: return fill_plan<Cfg5<0>>(p, which, N, K, OH, OW);
+    case 11: return fill_plan<Cfg1<0>>(p, which, N, K, OH, OW);
+    case 12: return fill_plan<Cfg2<0>>(p, which, N, K, OH, OW);
+    case 6: return fill_plan<Cfg6<0>>(p, which, N, K, OH, OW);
+    case 17: return fill_plan<Cfg7<0>>(p, which, N, K, OH, OW);
+    default: return fill_plan<Cfg7<0>>(p, which, N, K, OH, OW);
+  }
 }
 
 // Shared body of the fused ECR / PECR entries.
@@ -403,7 +454,15 @@ int sconv_cu_ctx_set_stream(sconv_cu_ctx* ctx, void* stream) {
   if (!ctx) return SCONV_ERR_ARG;
   DeviceGuard guard(ctx->device);
   CK(cudaStreamSynchronize(ctx->stream));  // workspace is stream-ordered
-  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return SCONV_OK;
+}
+
+int sconv_cu_ctx_use_own_stream(sconv_cu_ctx* ctx) {
+  if (!ctx) return SCONV_ERR_ARG;
+  DeviceGuard guard(ctx->device);
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->stream = ctx->own;
   return SCONV_OK;
 }
 
@@ -449,10 +508,8 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
     P = (pool_w == pool_h && pool_w == pool_stride) ? pool_w : -1;
   }
   const int which = (flags & SCONV_F_GENERIC) ? 0 : pick_tiled(k, kh, kw, stride, P);
-  if (which == 1) {
-    fill_plan<Cfg3x3R4<0>>(out, which, n, k, OH, OW);
-  } else if (which == 2) {
-    fill_plan<Cfg3x3R2<0>>(out, which, n, k, OH, OW);
+  if (which) {
+    plan_for(out, which, n, k, OH, OW);
   } else {
     const size_t work = size_t(n) * k * PHo * PWo;
     out->kernel = 0;

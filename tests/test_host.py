@@ -110,9 +110,9 @@ def test_shard_partition(sc):
 
 def test_launch_plan(sc):
     p = sc.launch_plan(64, 256, 58, 58, 256, 3, 3, 1)
-    assert p["kernel"] == 1 and p["grid_z"] == 64 and p["grid_y"] == 2 and p["block_threads"] == 128
+    assert p["kernel"] == 2 and p["grid_z"] == 64 and p["grid_y"] == 2 and p["block_threads"] == 256
     p = sc.launch_plan(64, 64, 226, 226, 64, 3, 3, 1, sc.PoolConfig(2, 2, 2))
-    assert p["kernel"] == 2 and p["smem_bytes"] <= 227 * 1024
+    assert p["kernel"] == 4 and p["smem_bytes"] <= 227 * 1024
     assert sc.launch_plan(1, 20, 11, 11, 50, 5, 5, 1)["kernel"] == 0
 
 
