@@ -321,3 +321,36 @@ def test_determinism(sc, orc):
     a = sc.ecr_conv_batched(x, f, 1, fast=True)
     for _ in range(3):
         assert bits_equal(sc.ecr_conv_batched(x, f, 1, fast=True), a)
+
+
+# ---------------------------------------------------------------------------
+# full-size VGG-19 layers: sampled (image, filter) pairs against the oracle
+# ---------------------------------------------------------------------------
+VGG_FULL = [("conv1_1", 3, 64, 224, False), ("conv1_2", 64, 64, 224, True),
+            ("conv2_2", 128, 128, 112, True), ("conv3_2", 256, 256, 56, False),
+            ("conv4_4", 512, 512, 28, True), ("conv5_1", 512, 512, 14, False)]
+
+
+@pytest.mark.parametrize("layer", VGG_FULL, ids=[v[0] for v in VGG_FULL])
+def test_vgg_full_size_sampled(sc, orc, layer):
+    """Full layer on the GPU (N=2, all K filters, reference generator inputs,
+    sparsity 0.7); filters {0, 1, K/2, K-1} of both images checked against the
+    oracle: EXACT bit-exact, FAST within 1e-5 + 1e-5|ref|."""
+    name, C, K, H, pooled = layer
+    l = [v[0] for v in VGG_FULL].index(name)
+    x = sc.generate_batch([1000 * l + n for n in range(2)], H + 2, H + 2, C, 0.7)
+    w = sc.generate_batch([5000 * l + k for k in range(K)], 3, 3, C, 0.0) - np.float32(0.5)
+    ks = [0, 1, K // 2, K - 1]
+    pool = sc.PoolConfig(2, 2, 2)
+    for fast in (False, True):
+        if pooled:
+            y = sc.pecr_conv_pool_batched(x, w, 1, pool, fast=fast)
+            ref, _ = orc.pecr_conv(x, w[ks], 1, 2, 2, 2, 0)
+        else:
+            y = sc.ecr_conv_batched(x, w, 1, fast=fast)
+            ref, _ = orc.ecr_conv(x, w[ks], 1)
+        got = y[:, ks]
+        if fast:
+            assert close(got, ref)
+        else:
+            assert bits_equal(got, ref)
