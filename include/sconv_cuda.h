@@ -61,6 +61,10 @@ typedef enum {
 #define SCONV_F_ASYNC (1u << 2)
 /* Force the generic (one thread per output) kernels; testing only. */
 #define SCONV_F_GENERIC (1u << 3)
+/* Force one tiled kernel configuration (testing / tuning only; ignored when
+ * the shape is not tileable): 1..6 = v2 TiledCfg1..6, 'A'..'D' = v3 WsA..D.
+ * 0 (default) lets the launch layer pick. */
+#define SCONV_F_KERNEL(id) (((unsigned)(id) & 0xffu) << 8)
 
 typedef enum { SCONV_POOL_MAX = 0, SCONV_POOL_MEAN = 1 } sconv_pool_mode;
 

@@ -32,6 +32,13 @@ F_DEVICE = 1 << 1
 F_ASYNC = 1 << 2
 F_GENERIC = 1 << 3
 
+
+def F_KERNEL(kid) -> int:
+    """SCONV_F_KERNEL: force a tiled configuration (1..6 v2, 'A'..'D' v3)."""
+    if isinstance(kid, str):
+        kid = ord(kid)
+    return (int(kid) & 0xFF) << 8
+
 _vp = C.c_void_p
 _i = C.c_int
 _u64p = C.POINTER(C.c_uint64)

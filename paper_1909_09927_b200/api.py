@@ -473,9 +473,11 @@ def _is_torch_cuda(t) -> bool:
 
 
 def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, counters,
-             device: Optional[int], generic: bool, out, sync: bool):
+             device: Optional[int], generic: bool, out, sync: bool, kernel=0):
     L = nat.lib()
     flags = (nat.F_FAST if fast else 0) | (nat.F_GENERIC if generic else 0)
+    if kernel:
+        flags |= nat.F_KERNEL(kernel)
     if _is_torch_cuda(x):
         import torch
         if not (_is_torch_cuda(filters) and x.dtype == torch.float32 and filters.dtype == torch.float32):
@@ -540,24 +542,25 @@ def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, co
 
 def ecr_conv_batched(x, filters, stride: int = 1, *, fast: bool = False,
                      counters: Optional[OpCount] = None, device: Optional[int] = None,
-                     generic: bool = False, out=None, sync: bool = True):
+                     generic: bool = False, out=None, sync: bool = True, kernel=0):
     """Fused ECR convolution of x [N,C,H,W] by filters [K,C,kh,kw] -> [N,K,oh,ow].
 
     Equivalent to multichannel_conv(map, filters, {stride}, Method::kEcr) per
     image (pipeline.cpp:191-210).  numpy in -> numpy out (host copies inside);
-    torch CUDA tensors in -> torch out on the current stream.
+    torch CUDA tensors in -> torch out on the current stream.  `kernel`
+    forces a tiled configuration (testing / tuning; SCONV_F_KERNEL).
     """
     return _batched("ecr", x, filters, stride, None, 0, fast, counters, device, generic, out,
-                    sync)
+                    sync, kernel)
 
 
 def pecr_conv_pool_batched(x, filters, stride: int = 1, pool: PoolConfig = PoolConfig(2, 2, 2),
                            *, fast: bool = False, counters: Optional[OpCount] = None,
                            device: Optional[int] = None, generic: bool = False, out=None,
-                           sync: bool = True):
+                           sync: bool = True, kernel=0):
     """Fused conv + ReLU + pooling (forward's fused branch, pipeline.cpp:249-264)."""
     return _batched("pecr", x, filters, stride, (pool.width, pool.height, pool.stride),
-                    int(pool.mode), fast, counters, device, generic, out, sync)
+                    int(pool.mode), fast, counters, device, generic, out, sync, kernel)
 
 
 def multichannel_conv(map: FeatureMap, filters: Sequence[Filter], cfg: ConvConfig,

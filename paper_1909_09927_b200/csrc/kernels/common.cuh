@@ -21,6 +21,27 @@ __device__ __forceinline__ float mac(float acc, float a, float b) {
   }
 }
 
+// Two FAST terms in one packed FFMA2 (sm_100a `fma.rn.f32x2`, the scalar
+// operand broadcast to both halves): {a0,a1} += {w0,w1} * v.  Same rounding
+// as two FFMAs; one issue slot instead of two, which leaves room for the
+// zero-skip branches of the ECR main loop.
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float w0, float w1, float v) {
+  asm("{\n\t.reg .b64 a, w, v;\n\t"
+      "mov.b64 a, {%0, %1};\n\t"
+      "mov.b64 w, {%2, %3};\n\t"
+      "mov.b64 v, {%4, %4};\n\t"
+      "fma.rn.f32x2 a, w, v, a;\n\t"
+      "mov.b64 {%0, %1}, a;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(w0), "f"(w1), "f"(v));
+}
+
+// Keeps ptxas from if-converting a zero-skip block into predicated FMAs
+// (which would issue -- and occupy the FMA pipe -- for every zero too).  It
+// emits one PMTRIG, which touches no registers; ptxas will not predicate a
+// block that holds it, so the block stays behind a uniform BRA.U.
+#define SCONV_KEEP_BRANCH() asm volatile("pmevent 0;")
+
 // Pooling fold of pecr_conv_pool (src/pecr.cpp:147-167).
 struct PoolFold {
   float best = 0.0f;  // max mode: running max starts at +0.0 -> ReLU folded

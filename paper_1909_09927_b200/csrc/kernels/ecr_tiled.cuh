@@ -254,9 +254,16 @@ __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArg
               for (int j = 0; j < KW; ++j) {
                 const int dx = X - j;
                 if (dx < 0 || dx % S != 0 || dx / S >= TW) continue;
+                if constexpr (FAST && R % 2 == 0) {
 #pragma unroll
-                for (int r = 0; r < R; ++r)
-                  acc[dy / S][dx / S][r] = mac<FAST>(acc[dy / S][dx / S][r], v, wr[i * KW + j][r]);
+                  for (int r = 0; r < R; r += 2)
+                    ffma2(acc[dy / S][dx / S][r], acc[dy / S][dx / S][r + 1], wr[i * KW + j][r],
+                          wr[i * KW + j][r + 1], v);
+                } else {
+#pragma unroll
+                  for (int r = 0; r < R; ++r)
+                    acc[dy / S][dx / S][r] = mac<FAST>(acc[dy / S][dx / S][r], v, wr[i * KW + j][r]);
+                }
               }
             }
           }

@@ -1,0 +1,358 @@
+// ecr_ws.cuh -- the hot path, v3: warp-specialised fused ECR compaction +
+// sparse convolution (+ the PECR ReLU/pooling epilogue) for sm_100a.
+//
+// Same arithmetic as ecr_tiled.cuh (input-stationary, lanes over output
+// channels, warp-uniform zero skip, terms in (c, i, j) order per output), but
+// the CTA is organised around what the B200 profile of v2 showed:
+//
+// * One producer warp stages CC-channel chunks into an NS-deep ring of
+//   shared-memory stages with cp.async and signals a `full` mbarrier
+//   (cp.async.mbarrier.arrive.noinc); consumer warps release a stage through
+//   an `empty` mbarrier.  There is no __syncthreads in the main loop, so a
+//   warp whose tiles happen to be denser than its neighbours' no longer
+//   stalls the CTA at every chunk (v2: ~13-17% of stall samples were
+//   barrier), and the consumers execute no staging address arithmetic.
+// * Each consumer warp owns one TH x TW output tile of any image; the
+//   producer copies that warp's (TH-1)S+KH x (TW-1)S+KW input window into a
+//   private, 16B-aligned sub-patch (halo columns duplicated).  Tiles are a
+//   flat list over (image, tile) so any tile shape covers any map size with
+//   no partial-tile waste (v2 computed 32x32 for the 28x28 layers).
+// * FAST mode multiplies with packed FFMA2 (fma.rn.f32x2, the input value
+//   broadcast to both halves): half the FMA instructions of v2 and no
+//   even/odd register-bank conflicts between weight and accumulator.
+//
+// Bit-exactness in EXACT mode is unchanged: per output, terms arrive in
+// channel order (chunks ascend, channels inside a chunk ascend) and within a
+// channel in window raster order, i.e. the order of ecr_convert's f_data /
+// k_data (src/ecr.cpp:79-91) summed as in ecr_spmv_conv (:117-120).
+#pragma once
+
+#include "common.cuh"
+
+namespace sconv_cu {
+
+template <int KH_, int KW_, int S_, int TH_, int TW_, int R_, int WPC_, int CC_, int NS_, int P_>
+struct WsCfg {
+  static constexpr int KH = KH_, KW = KW_, S = S_, TH = TH_, TW = TW_, R = R_;
+  static constexpr int WPC = WPC_, CC = CC_, NS = NS_, P = P_;
+  static constexpr int KK = KH * KW;
+  static constexpr int KT = 32 * R;                  // output channels per CTA
+  static constexpr int WPH = (TH - 1) * S + KH;      // warp input window rows
+  static constexpr int WPW = (TW - 1) * S + KW;      // warp input window cols
+  static constexpr int PITCH = WPW <= 8 ? 8 : 16;    // sub-patch row pitch (floats)
+  static constexpr int PATCH = WPH * PITCH;          // floats per (warp, channel)
+  static constexpr int NPOS = WPH * WPW;
+  static constexpr int IN_STAGE = WPC * CC * PATCH;  // floats
+  static constexpr int W_STAGE = CC * KK * KT;       // floats
+  static constexpr int STAGE = IN_STAGE + W_STAGE;
+  static constexpr int NT = 32 * (WPC + 1);          // + producer warp
+  static constexpr int MINB = NT > 256 ? 1 : (TH * TW * R <= 32 ? 3 : 2);  // CTAs per SM
+  static constexpr int SMEM_BYTES = NS * STAGE * 4 + 2 * NS * 8;
+  static constexpr int CELLS = WPC * NPOS;           // input cells per channel
+  static constexpr int CELLS_PER_LANE = (CELLS + 31) / 32;
+  static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
+  static_assert(R == 2 || R == 4 || R == 8, "R");
+  static_assert(P == 0 || (TH % P == 0 && TW % P == 0), "pool tile");
+  static_assert((IN_STAGE * 4) % 16 == 0, "weight region must stay 16B aligned");
+};
+
+struct WsArgs {
+  const float* x;   // [N][C][H][W]
+  const float* wt;  // [C][KH*KW][Kp]  (filters transposed once per call)
+  float* y;         // [N][K][OH][OW] or pooled [N][K][OH/P][OW/P]
+  int N, C, H, W, K, Kp, OH, OW;
+  int tiles_x, tiles_per_img, total_tiles;
+  int mode;  // pool mode (P > 0)
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  while (!mbar_try_wait(b, parity)) __nanosleep(32);
+}
+// The producer runs ahead and mostly waits for the slowest consumer warp:
+// back off instead of spinning, a polling warp steals issue slots from the
+// consumer warps on its SMSP.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
+  while (!mbar_try_wait(b, parity)) __nanosleep(256);
+}
+
+template <int R>
+__device__ __forceinline__ int ws_lane_chan(int lane, int r) {
+  if constexpr (R >= 4) {
+    return (r / 4) * 128 + lane * 4 + (r % 4);
+  } else {
+    return lane * R + r;
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void ws_lds_w(float (&dst)[R], const float* row, int lane) {
+  if constexpr (R >= 4) {
+#pragma unroll
+    for (int g = 0; g < R / 4; ++g) {
+      const float4 a = *reinterpret_cast<const float4*>(row + g * 128 + lane * 4);
+      dst[4 * g + 0] = a.x;
+      dst[4 * g + 1] = a.y;
+      dst[4 * g + 2] = a.z;
+      dst[4 * g + 3] = a.w;
+    }
+  } else {
+    const float2 a = *reinterpret_cast<const float2*>(row + lane * 2);
+    dst[0] = a.x;
+    dst[1] = a.y;
+  }
+}
+
+// Keeps a zero-skip block behind its uniform branch (see SCONV_KEEP_BRANCH);
+// __syncwarp emits no instruction in converged code but is not if-converted,
+// and it lets ptxas batch the mask-bit predicates ahead of the branches.
+#ifndef SCONV_WS_GUARD
+#define SCONV_WS_GUARD 2
+#endif
+
+template <class Cfg, bool FAST>
+__global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) ecr_ws_kernel(const WsArgs a) {
+  constexpr int KH = Cfg::KH, KW = Cfg::KW, S = Cfg::S, TH = Cfg::TH, TW = Cfg::TW, R = Cfg::R;
+  constexpr int KK = Cfg::KK, KT = Cfg::KT, CC = Cfg::CC, NS = Cfg::NS, P = Cfg::P;
+  constexpr int WPC = Cfg::WPC, WPH = Cfg::WPH, WPW = Cfg::WPW, PITCH = Cfg::PITCH;
+  constexpr int PATCH = Cfg::PATCH;
+
+  extern __shared__ float4 smem_raw[];
+  float* smem = reinterpret_cast<float*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * Cfg::STAGE);
+  uint64_t* empty = full + NS;
+
+  const int tid = threadIdx.x;
+  // The shuffle makes the warp index provably warp-uniform to ptxas: with a
+  // plain tid >> 5 the role split below is a "divergent" branch, the ballot
+  // masks land in vector registers and every zero-skip branch pays a vector
+  // bit test right before it (plus BRA.DIV checks for the guard).
+  const int warp = __shfl_sync(kFull, tid >> 5, 0), lane = tid & 31;
+  const int k0 = blockIdx.y * KT;
+  const int C = a.C, H = a.H, W = a.W, K = a.K;
+  const int nchunks = (C + CC - 1) / CC;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], WPC);
+    }
+  }
+  __syncthreads();
+
+  if (warp == WPC) {
+    // ------------------------------ producer ------------------------------
+    const size_t plane = static_cast<size_t>(H) * W;
+    int src_off[Cfg::CELLS_PER_LANE];
+    int dst_off[Cfg::CELLS_PER_LANE];
+    bool ok[Cfg::CELLS_PER_LANE];
+#pragma unroll
+    for (int e = 0; e < Cfg::CELLS_PER_LANE; ++e) {
+      const int q = lane + 32 * e;
+      const int wi = q / Cfg::NPOS, pos = q - (q / Cfg::NPOS) * Cfg::NPOS;
+      const int Y = pos / WPW, X = pos - (pos / WPW) * WPW;
+      const int t = blockIdx.x * WPC + wi;
+      const int n = t / a.tiles_per_img, tt = t - n * a.tiles_per_img;
+      const int ty = tt / a.tiles_x, tx = tt - ty * a.tiles_x;
+      const int iy = ty * TH * S + Y, ix = tx * TW * S + X;
+      ok[e] = q < Cfg::CELLS && t < a.total_tiles && iy < H && ix < W;
+      src_off[e] = ok[e] ? static_cast<int>((static_cast<size_t>(n) * C * H + iy) * W + ix) : 0;
+      dst_off[e] = (wi * CC) * PATCH + Y * PITCH + X;
+    }
+    constexpr int QW = KT / 4;  // 16B pieces per weight row
+    for (int k = 0; k < nchunks; ++k) {
+      const int s = k % NS;
+      if (k >= NS) mbar_wait_sleep(&empty[s], ((k / NS) + 1) & 1);
+      float* in_s = smem + s * Cfg::STAGE;
+      float* w_s = in_s + Cfg::IN_STAGE;
+      const int c0 = k * CC;
+#pragma unroll
+      for (int e = 0; e < Cfg::CELLS_PER_LANE; ++e) {
+        if (lane + 32 * e < Cfg::CELLS) {
+#pragma unroll
+          for (int ch = 0; ch < CC; ++ch) {
+            const bool v = ok[e] && c0 + ch < C;
+            const float* src = v ? a.x + src_off[e] + (c0 + ch) * plane : a.x;
+            cp_async4(in_s + dst_off[e] + ch * PATCH, src, v);
+          }
+        }
+      }
+      for (int idx = lane; idx < CC * KK * QW; idx += 32) {
+        const int row = idx / QW, q = idx - row * QW;
+        const int ch = row / KK;
+        const bool v = c0 + ch < C && k0 + 4 * q < a.Kp;
+        const float* src =
+            v ? a.wt + (static_cast<size_t>(c0) * KK + row) * a.Kp + k0 + 4 * q : a.wt;
+        cp_async16(w_s + row * KT + 4 * q, src, v);
+      }
+      mbar_arrive_cp_async(&full[s]);
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  // ------------------------------- consumers -------------------------------
+  const int t = blockIdx.x * WPC + warp;
+  const bool active = t < a.total_tiles;
+  const int n = active ? t / a.tiles_per_img : 0;
+  const int tt = t - n * a.tiles_per_img;
+  const int ty = tt / a.tiles_x, tx = tt - (tt / a.tiles_x) * a.tiles_x;
+
+  float acc[TH][TW][R];
+#pragma unroll
+  for (int i = 0; i < TH; ++i)
+#pragma unroll
+    for (int j = 0; j < TW; ++j)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[i][j][r] = 0.0f;
+
+  // Lane l tests sub-patch cells l and l+32 (bit = Y*PITCH + X).
+  const bool t0 = (lane % PITCH) < WPW && (lane / PITCH) < WPH;
+  const bool t1 = ((lane + 32) % PITCH) < WPW && ((lane + 32) / PITCH) < WPH;
+  constexpr bool TWO = WPH * PITCH > 32;
+
+  for (int k = 0; k < nchunks; ++k) {
+    const int s = k % NS;
+    mbar_wait(&full[s], (k / NS) & 1);
+    if (active) {
+      const float* ic = smem + s * Cfg::STAGE + warp * CC * PATCH;
+      const float* wsrc = smem + s * Cfg::STAGE + Cfg::IN_STAGE;
+      const int cn = min(CC, C - k * CC);
+#pragma unroll 1
+      for (int c = 0; c < cn; ++c, ic += PATCH, wsrc += KK * KT) {
+        const unsigned m0 = __ballot_sync(kFull, t0 && ic[lane] != 0.0f);
+        const unsigned m1 = TWO ? __ballot_sync(kFull, t1 && ic[lane + 32] != 0.0f) : 0u;
+
+        float wr[KK][R];
+#pragma unroll
+        for (int ij = 0; ij < KK; ++ij) ws_lds_w<R>(wr[ij], wsrc + ij * KT, lane);
+
+#pragma unroll
+        for (int Y = 0; Y < WPH; ++Y) {
+          constexpr int W4 = (WPW + 3) / 4;
+          float row[4 * W4];
+#pragma unroll
+          for (int q = 0; q < W4; ++q) {
+            const float4 v4 = *reinterpret_cast<const float4*>(ic + Y * PITCH + 4 * q);
+            row[4 * q + 0] = v4.x;
+            row[4 * q + 1] = v4.y;
+            row[4 * q + 2] = v4.z;
+            row[4 * q + 3] = v4.w;
+          }
+#pragma unroll
+          for (int X = 0; X < WPW; ++X) {
+            const int b = Y * PITCH + X;
+            const bool nz = b < 32 ? ((m0 >> b) & 1u) : ((m1 >> (b - 32)) & 1u);
+            if (nz) {  // warp-uniform: the mask came from a ballot
+#if SCONV_WS_GUARD == 1
+              SCONV_KEEP_BRANCH();
+#elif SCONV_WS_GUARD == 2
+              __syncwarp();
+#endif
+              const float v = row[X];
+#pragma unroll
+              for (int i = 0; i < KH; ++i) {
+                const int dy = Y - i;
+                if (dy < 0 || dy % S != 0 || dy / S >= TH) continue;
+#pragma unroll
+                for (int j = 0; j < KW; ++j) {
+                  const int dx = X - j;
+                  if (dx < 0 || dx % S != 0 || dx / S >= TW) continue;
+                  if constexpr (FAST) {
+#pragma unroll
+                    for (int r = 0; r < R; r += 2)
+                      ffma2(acc[dy / S][dx / S][r], acc[dy / S][dx / S][r + 1], wr[i * KW + j][r],
+                            wr[i * KW + j][r + 1], v);
+                  } else {
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                      acc[dy / S][dx / S][r] = mac<false>(acc[dy / S][dx / S][r], v, wr[i * KW + j][r]);
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (!active) return;
+
+  // ---- epilogue ------------------------------------------------------------
+  const int oy0 = ty * TH, ox0 = tx * TW;
+  if constexpr (P == 0) {
+    const bool vec = (TW % 4 == 0) && (a.OW % 4 == 0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int kk = k0 + ws_lane_chan<R>(lane, r);
+      if (kk >= K) continue;
+      float* dst = a.y + ((static_cast<size_t>(n) * K + kk) * a.OH + oy0) * a.OW + ox0;
+#pragma unroll
+      for (int oy = 0; oy < TH; ++oy) {
+        if (oy0 + oy >= a.OH) continue;
+        if (vec) {
+#pragma unroll
+          for (int q = 0; q < TW / 4; ++q)
+            if (ox0 + 4 * q < a.OW)
+              *reinterpret_cast<float4*>(dst + oy * a.OW + 4 * q) =
+                  make_float4(acc[oy][4 * q][r], acc[oy][4 * q + 1][r], acc[oy][4 * q + 2][r],
+                              acc[oy][4 * q + 3][r]);
+        } else {
+#pragma unroll
+          for (int ox = 0; ox < TW; ++ox)
+            if (ox0 + ox < a.OW) dst[oy * a.OW + ox] = acc[oy][ox][r];
+        }
+      }
+    }
+  } else {
+    const int PHo = a.OH / P, PWo = a.OW / P;
+    const int py0 = oy0 / P, px0 = ox0 / P;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int kk = k0 + ws_lane_chan<R>(lane, r);
+      if (kk >= K) continue;
+      float* dst = a.y + ((static_cast<size_t>(n) * K + kk) * PHo + py0) * PWo + px0;
+#pragma unroll
+      for (int py = 0; py < TH / P; ++py) {
+        if (py0 + py >= PHo) continue;
+#pragma unroll
+        for (int px = 0; px < TW / P; ++px) {
+          if (px0 + px >= PWo) continue;
+          PoolFold f;
+#pragma unroll
+          for (int u = 0; u < P; ++u)
+#pragma unroll
+            for (int v = 0; v < P; ++v) f.add(acc[py * P + u][px * P + v][r], a.mode);
+          dst[py * PWo + px] = f.result(a.mode, P * P);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace sconv_cu

@@ -73,15 +73,16 @@ __global__ void pecr_generic_kernel(const GenericArgs a) {
   }
 }
 
-// Filter re-layout for the tiled kernel: wt[c][i*kw+j][k] = w[k][c][i][j].
+// Filter re-layout for the tiled kernels: wt[c][i*kw+j][k] = w[k][c][i][j],
+// rows padded to Kp >= K output channels with zeros (16B-aligned rows).
 __global__ void transpose_filters_kernel(const float* __restrict__ w, float* __restrict__ wt, int K,
-                                         int C, int KK) {
-  const size_t total = static_cast<size_t>(K) * C * KK;
+                                         int Kp, int C, int KK) {
+  const size_t total = static_cast<size_t>(Kp) * C * KK;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const int k = static_cast<int>(idx % K);
-    const size_t cij = idx / K;  // c*KK + ij
-    wt[idx] = __ldg(w + static_cast<size_t>(k) * C * KK + cij);
+    const int k = static_cast<int>(idx % Kp);
+    const size_t cij = idx / Kp;  // c*KK + ij
+    wt[idx] = k < K ? __ldg(w + static_cast<size_t>(k) * C * KK + cij) : 0.0f;
   }
 }
 

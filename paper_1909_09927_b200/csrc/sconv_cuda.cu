@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "kernels/ecr_tiled.cuh"
+#include "kernels/ecr_ws.cuh"
 #include "kernels/format.cuh"
 #include "kernels/generic.cuh"
 #include "sconv_cuda.h"
@@ -251,6 +252,81 @@ void plan_for(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// v3 warp-specialised kernel registry (kernels/ecr_ws.cuh).  WsCfg<KH, KW, S,
+// TH, TW, R, WPC, CC, NS, P>: warp tile TH x TW outputs x 32R channels, WPC
+// consumer warps + 1 producer warp, CC channels per stage, NS stages.
+// ---------------------------------------------------------------------------
+// 7 consumer warps + the producer = 8 warps, two CTAs per SM.
+template <int P> using WsA = WsCfg<3, 3, 1, 4, 4, 4, 7, 4, 4, P>;  // K >= 128
+template <int P> using WsB = WsCfg<3, 3, 1, 2, 7, 4, 7, 4, 4, P>;  // 14-wide maps, K >= 128
+template <int P> using WsC = WsCfg<3, 3, 1, 4, 6, 2, 7, 4, 4, P>;  // K = 64
+template <int P> using WsD = WsCfg<3, 3, 1, 2, 4, 4, 7, 4, 3, P>;  // small tiles, 3 CTAs/SM
+
+template <class Cfg, bool FAST>
+int launch_ws_cfg(sconv_cu_ctx* ctx, const WsArgs& a0) {
+  auto kern = ecr_ws_kernel<Cfg, FAST>;
+  static bool attr_done[64] = {};
+  const int slot = ctx->device & 63;
+  if (!attr_done[slot]) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_done[slot] = true;
+  }
+  WsArgs a = a0;
+  a.tiles_x = (a.OW + Cfg::TW - 1) / Cfg::TW;
+  a.tiles_per_img = a.tiles_x * ((a.OH + Cfg::TH - 1) / Cfg::TH);
+  a.total_tiles = a.tiles_per_img * a.N;
+  dim3 grid((a.total_tiles + Cfg::WPC - 1) / Cfg::WPC, (a.K + Cfg::KT - 1) / Cfg::KT);
+  kern<<<grid, Cfg::NT, Cfg::SMEM_BYTES, ctx->stream>>>(a);
+  return finish_launch(ctx, "ecr_ws_kernel");
+}
+
+// which ws config (0 = none); P is 0 (ECR) or 2 (PECR 2x2/2)
+int pick_ws(int K, int OW, int kh, int kw, int S, int P) {
+  if (!(kh == 3 && kw == 3 && S == 1 && (P == 0 || P == 2) && K >= 32)) return 0;
+  const char* e = std::getenv("SCONV_KERNEL");
+  if (e && std::strcmp(e, "v2") == 0) return 0;
+  if (e && e[0] == 'w' && e[1] >= 'A' && e[1] <= 'D') return e[1] - 'A' + 1;
+  if (e && std::strcmp(e, "v3") == 0) {
+    if (K <= 64) return 3;
+    if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
+    return 1;
+  }
+  // Measured on B200 (tools/tune.py, profiles/r01): v3 wins on the K = 512
+  // layers (conv4_x / conv5_x: 5-6% faster, no partial tiles), v2 on the
+  // shallower ones, where v3's per-CTA producer pipeline start-up is not
+  // amortised over enough channel chunks.
+  if (K < 512) return 0;
+  if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
+  return 1;
+}
+
+template <bool FAST>
+int launch_ws(sconv_cu_ctx* ctx, int which, int P, const WsArgs& a) {
+  switch (which) {
+    case 1: return P ? launch_ws_cfg<WsA<2>, FAST>(ctx, a) : launch_ws_cfg<WsA<0>, FAST>(ctx, a);
+    case 2: return launch_ws_cfg<WsB<0>, FAST>(ctx, a);
+    case 4: return P ? launch_ws_cfg<WsD<2>, FAST>(ctx, a) : launch_ws_cfg<WsD<0>, FAST>(ctx, a);
+    default: return P ? launch_ws_cfg<WsC<2>, FAST>(ctx, a) : launch_ws_cfg<WsC<0>, FAST>(ctx, a);
+  }
+}
+
+// Plan of a v3 launch: kernel id 100 + registry index; grid_x counts CTAs of
+// WPC warp tiles over the flat (image, tile) list, grid_z is 1.
+template <class Cfg>
+void plan_ws(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
+  const long tiles = long((OH + Cfg::TH - 1) / Cfg::TH) * ((OW + Cfg::TW - 1) / Cfg::TW) * N;
+  p->kernel = 100 + which;
+  p->grid_x = static_cast<int>((tiles + Cfg::WPC - 1) / Cfg::WPC);
+  p->grid_y = (K + Cfg::KT - 1) / Cfg::KT;
+  p->grid_z = 1;
+  p->block_threads = Cfg::NT;
+  p->smem_bytes = Cfg::SMEM_BYTES;
+  p->tile_h = Cfg::TH;
+  p->tile_w = Cfg::TW;
+  p->tile_k = Cfg::KT;
+}
+
 // Shared body of the fused ECR / PECR entries.
 int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, const float* filt,
                int k, int kh, int kw, int stride, int pw, int ph, int ps, int mode, float* y,
@@ -278,7 +354,23 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   const size_t y_elems = pecr ? size_t(n) * k * PHo * PWo : size_t(n) * k * OH * OW;
   int P = 0;
   if (pecr && pw == ph && pw == ps) P = pw;
-  const int which = (flags & SCONV_F_GENERIC) ? 0 : pick_tiled(k, kh, kw, stride, pecr ? (P ? P : -1) : 0);
+  const int Pk = pecr ? (P ? P : -1) : 0;
+  int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, OW, kh, kw, stride, Pk);
+  int which = (flags & SCONV_F_GENERIC) || ws ? 0 : pick_tiled(k, kh, kw, stride, Pk);
+  const int forced = (flags >> 8) & 0xff;
+  const bool tileable = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
+  if (forced && tileable && !(flags & SCONV_F_GENERIC)) {
+    if (forced >= 1 && forced <= kNumCfgs) {
+      which = forced;
+      ws = 0;
+    } else if (forced >= 'A' && forced <= 'D' && !(forced == 'B' && Pk != 0)) {
+      ws = forced - 'A' + 1;
+      which = 0;
+    } else {
+      return fail(ctx, SCONV_ERR_ARG, "unknown forced kernel id %d", forced);
+    }
+  }
+  const int Kp = (k + 3) / 4 * 4;
   const bool counters = muls || adds;
 
   DeviceGuard guard(ctx->device);
@@ -286,7 +378,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   const size_t i_x = dev ? 0 : ar.add(x_elems * 4);
   const size_t i_w = dev ? 0 : ar.add(w_elems * 4);
   const size_t i_y = dev ? 0 : ar.add(y_elems * 4);
-  const size_t i_wt = which ? ar.add(w_elems * 4) : 0;
+  const size_t i_wt = (which || ws) ? ar.add(size_t(Kp) * c * kh * kw * 4) : 0;
   const size_t i_pix = counters ? ar.add(size_t(n) * h * w * 4) : 0;
   const size_t i_ops = ar.add(64);
   std::vector<char*> p;
@@ -302,9 +394,16 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     CK(cudaMemcpyAsync(const_cast<float*>(dw), filt, w_elems * 4, cudaMemcpyHostToDevice, st));
   }
 
-  if (which) {
+  if (ws) {
     float* wt = reinterpret_cast<float*>(p[i_wt]);
-    transpose_filters_kernel<<<grid_for(w_elems, 256, ctx->num_sms), 256, 0, st>>>(dw, wt, k, c,
+    transpose_filters_kernel<<<grid_for(size_t(Kp) * c * kh * kw, 256, ctx->num_sms), 256, 0, st>>>(
+        dw, wt, k, Kp, c, kh * kw);
+    TRY(finish_launch(ctx, "transpose_filters_kernel"));
+    WsArgs a{dx, wt, dy, n, c, h, w, k, Kp, OH, OW, 0, 0, 0, mode};
+    TRY(fast ? launch_ws<true>(ctx, ws, P, a) : launch_ws<false>(ctx, ws, P, a));
+  } else if (which) {
+    float* wt = reinterpret_cast<float*>(p[i_wt]);
+    transpose_filters_kernel<<<grid_for(w_elems, 256, ctx->num_sms), 256, 0, st>>>(dw, wt, k, k, c,
                                                                                     kh * kw);
     TRY(finish_launch(ctx, "transpose_filters_kernel"));
     TiledArgs a{dx, wt, dy, c, h, w, k, OH, OW, 0, mode};
@@ -507,8 +606,16 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
     TRY(pack_count(nullptr, h, kh, stride, pool_h, pool_stride, &PHo));
     P = (pool_w == pool_h && pool_w == pool_stride) ? pool_w : -1;
   }
-  const int which = (flags & SCONV_F_GENERIC) ? 0 : pick_tiled(k, kh, kw, stride, P);
-  if (which) {
+  const int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, OW, kh, kw, stride, P);
+  const int which = (flags & SCONV_F_GENERIC) || ws ? 0 : pick_tiled(k, kh, kw, stride, P);
+  if (ws) {
+    switch (ws) {
+      case 1: plan_ws<WsA<0>>(out, ws, n, k, OH, OW); break;
+      case 2: plan_ws<WsB<0>>(out, ws, n, k, OH, OW); break;
+      case 4: plan_ws<WsD<0>>(out, ws, n, k, OH, OW); break;
+      default: plan_ws<WsC<0>>(out, ws, n, k, OH, OW); break;
+    }
+  } else if (which) {
     plan_for(out, which, n, k, OH, OW);
   } else {
     const size_t work = size_t(n) * k * PHo * PWo;

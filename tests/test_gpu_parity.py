@@ -203,6 +203,42 @@ def test_pecr_fused(sc, orc, shape):
             assert bits_equal(y, sep)
 
 
+# ---------------------------------------------------------------------------
+# every tiled configuration, forced (SCONV_F_KERNEL), including the v3
+# warp-specialised kernel on K = 512 / 14-wide maps and ragged tile lists
+# ---------------------------------------------------------------------------
+
+KSHAPES = [
+    # n, c, h, w, k, sparsity
+    (2, 13, 16, 16, 512, 0.7),     # conv5-like 14x14, K tail-free
+    (3, 9, 30, 30, 160, 0.7),      # 28x28, K not a multiple of 128 (tail CTA)
+    (1, 11, 11, 19, 96, 0.5),      # ragged tiles in both directions
+    (2, 6, 10, 13, 64, 0.9),
+    (1, 5, 12, 12, 256, 1.0),      # all zero
+    (1, 7, 9, 9, 128, 0.0),        # dense
+]
+KERNELS = [1, 2, 3, 4, 5, 6, "A", "B", "C", "D"]
+
+
+@pytest.mark.parametrize("kid", KERNELS, ids=[str(k) for k in KERNELS])
+@pytest.mark.parametrize("shape", KSHAPES, ids=[str(s) for s in KSHAPES])
+def test_forced_kernels(sc, orc, shape, kid):
+    n, c, h, w, k, sp = shape
+    x, f = inputs(orc, n, c, h, w, k, 3, 3, sp, seed=(hash(shape) ^ 77) & 0xFFFF)
+    ref, _ = orc.ecr_conv(x, f, 1)
+    y = sc.ecr_conv_batched(x, f, 1, kernel=kid)
+    assert bits_equal(y, ref), f"ECR EXACT mismatch kernel={kid}"
+    assert close(sc.ecr_conv_batched(x, f, 1, fast=True, kernel=kid), ref)
+    if kid == "B" or (h - 2) % 2 or (w - 2) % 2:
+        return
+    for mode in (0, 1):
+        pref, _ = orc.pecr_conv(x, f, 1, 2, 2, 2, mode)
+        pool = sc.PoolConfig(2, 2, 2, sc.PoolMode(mode))
+        p = sc.pecr_conv_pool_batched(x, f, 1, pool, kernel=kid)
+        assert bits_equal(p, pref), f"PECR EXACT mismatch kernel={kid} mode={mode}"
+        assert close(sc.pecr_conv_pool_batched(x, f, 1, pool, fast=True, kernel=kid), pref)
+
+
 def test_errors(sc):
     x = np.ones((1, 2, 5, 5), np.float32)
     with pytest.raises(sc.ShapeError):

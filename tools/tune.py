@@ -26,6 +26,6 @@ for name, C, K, Ho in [("conv1_2",64,64,224),("conv2_2",128,128,112),("conv3_2",
 print(json.dumps(out))
 ''' % ROOT
 for cfg in sys.argv[1:] or ["1", "2", "3", "4", "5", "6"]:
-    env = dict(os.environ, SCONV_TILED_CFG=cfg)
+    env = dict(os.environ, SCONV_TILED_CFG=cfg) if cfg[0].isdigit() else dict(os.environ, SCONV_KERNEL=cfg)
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
     print("cfg", cfg, r.stdout.strip() or r.stderr[-500:], flush=True)
