@@ -62,7 +62,7 @@ typedef enum {
 /* Force the generic (one thread per output) kernels; testing only. */
 #define SCONV_F_GENERIC (1u << 3)
 /* Force one tiled kernel configuration (testing / tuning only; ignored when
- * the shape is not tileable): 1..6 = v2 TiledCfg1..6, 'A'..'D' = v3 WsA..D.
+ * the shape is not tileable): 1..6 = v2 TiledCfg1..6, 'A'..'G' = v3 WsA..G.
  * 0 (default) lets the launch layer pick. */
 #define SCONV_F_KERNEL(id) (((unsigned)(id) & 0xffu) << 8)
 

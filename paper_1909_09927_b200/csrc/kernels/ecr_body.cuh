@@ -1,0 +1,82 @@
+// ecr_body.cuh -- the per-channel ECR step shared by the v2 (ecr_tiled.cuh)
+// and v3 (ecr_ws.cuh) kernels.
+//
+// One warp, one input channel c, one TH x TW output tile: `is` points at the
+// warp's (TH-1)S+KH x (TW-1)S+KW input window of channel c in shared memory
+// (row pitch SPITCH floats, rows 16B aligned), and (m0, m1) is the window's
+// nonzero mask from two ballots, bit Y*BPITCH + X for window cell (Y, X).
+// That mask is the ECR compaction of the window (ecr_convert keeps exactly the
+// v != 0 cells, src/ecr.cpp:79-91); it is computed once per channel and
+// shared by all 32*R output channels of the warp.
+//
+// For every set bit, in window raster order, the cell value v is broadcast
+// and multiplied into each output whose 3x3 (KH x KW) window covers the cell,
+// against register-resident weights wr[i*KW+j][r]: for every output the
+// terms of channel c arrive in (i, j) order, so with EXACT arithmetic (rounded
+// mul, rounded add) the sum is bit-identical to ecr_spmv_conv (:117-120).
+// FAST uses packed FFMA2 (same order, fused rounding).
+//
+// The branch per cell is warp-uniform (the mask came from a ballot); its cost
+// (~4 SMSP cycles on B200, tools/micro/branch_cost.cu) is what bounds this
+// kernel.  ROWSKIP adds one test per window row and skips rows without a
+// nonzero: a win once fewer than ~1/4 of the cells are nonzero, so the
+// kernels select it per channel from the mask's popcount.
+#pragma once
+
+#include "common.cuh"
+
+namespace sconv_cu {
+
+template <int KH, int KW, int S, int TH, int TW, int R, int WPH, int WPW, int BPITCH, int SPITCH,
+          bool FAST, bool ROWSKIP, bool NOSKIP = false>
+__device__ __forceinline__ void ecr_channel(float (&acc)[TH][TW][R], const float (&wr)[KH * KW][R],
+                                            const float* is, unsigned m0, unsigned m1) {
+  static_assert(WPH * BPITCH <= 64, "window mask must fit 64 bits");
+  constexpr int W4 = (WPW + 3) / 4;
+  const unsigned long long mm = (static_cast<unsigned long long>(m1) << 32) | m0;
+#pragma unroll
+  for (int Y = 0; Y < WPH; ++Y) {
+    if constexpr (ROWSKIP) {
+      if (((mm >> (Y * BPITCH)) & ((1ull << WPW) - 1ull)) == 0ull) continue;  // empty row
+    }
+    float row[4 * W4];
+#pragma unroll
+    for (int q = 0; q < W4; ++q) {
+      const float4 v4 = *reinterpret_cast<const float4*>(is + Y * SPITCH + 4 * q);
+      row[4 * q + 0] = v4.x;
+      row[4 * q + 1] = v4.y;
+      row[4 * q + 2] = v4.z;
+      row[4 * q + 3] = v4.w;
+    }
+#pragma unroll
+    for (int X = 0; X < WPW; ++X) {
+      const int b = Y * BPITCH + X;
+      const bool nz = b < 32 ? ((m0 >> b) & 1u) : ((m1 >> (b - 32)) & 1u);
+      if (NOSKIP || nz) {  // warp-uniform
+        const float v = row[X];
+#pragma unroll
+        for (int i = 0; i < KH; ++i) {
+          const int dy = Y - i;
+          if (dy < 0 || dy % S != 0 || dy / S >= TH) continue;
+#pragma unroll
+          for (int j = 0; j < KW; ++j) {
+            const int dx = X - j;
+            if (dx < 0 || dx % S != 0 || dx / S >= TW) continue;
+            if constexpr (FAST && R % 2 == 0) {
+#pragma unroll
+              for (int r = 0; r < R; r += 2)
+                ffma2(acc[dy / S][dx / S][r], acc[dy / S][dx / S][r + 1], wr[i * KW + j][r],
+                      wr[i * KW + j][r + 1], v);
+            } else {
+#pragma unroll
+              for (int r = 0; r < R; ++r)
+                acc[dy / S][dx / S][r] = mac<FAST>(acc[dy / S][dx / S][r], v, wr[i * KW + j][r]);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace sconv_cu

@@ -31,6 +31,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "ecr_body.cuh"
 
 namespace sconv_cu {
 
@@ -229,46 +230,11 @@ __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArg
       for (int ij = 0; ij < KK; ++ij) lds_w<R>(wr[ij], wsrc + ij * KT, lane);
 
       const float* is = ic + wbase;
-#pragma unroll
-      for (int Y = 0; Y < WPH; ++Y) {
-        float row[WPW4];
-#pragma unroll
-        for (int q = 0; q < WPW4 / 4; ++q) {
-          const float4 v4 = *reinterpret_cast<const float4*>(is + Y * PWS + 4 * q);
-          row[4 * q + 0] = v4.x;
-          row[4 * q + 1] = v4.y;
-          row[4 * q + 2] = v4.z;
-          row[4 * q + 3] = v4.w;
-        }
-#pragma unroll
-        for (int X = 0; X < WPW; ++X) {
-          const int p = Y * WPW + X;
-          const bool nz = p < 32 ? ((m0 >> p) & 1u) : ((m1 >> (p - 32)) & 1u);
-          if (NOSKIP || nz) {  // uniform: the mask came from a ballot
-            const float v = row[X];
-#pragma unroll
-            for (int i = 0; i < KH; ++i) {
-              const int dy = Y - i;
-              if (dy < 0 || dy % S != 0 || dy / S >= TH) continue;
-#pragma unroll
-              for (int j = 0; j < KW; ++j) {
-                const int dx = X - j;
-                if (dx < 0 || dx % S != 0 || dx / S >= TW) continue;
-                if constexpr (FAST && R % 2 == 0) {
-#pragma unroll
-                  for (int r = 0; r < R; r += 2)
-                    ffma2(acc[dy / S][dx / S][r], acc[dy / S][dx / S][r + 1], wr[i * KW + j][r],
-                          wr[i * KW + j][r + 1], v);
-                } else {
-#pragma unroll
-                  for (int r = 0; r < R; ++r)
-                    acc[dy / S][dx / S][r] = mac<FAST>(acc[dy / S][dx / S][r], v, wr[i * KW + j][r]);
-                }
-              }
-            }
-          }
-        }
-      }
+      if (!NOSKIP && (__popc(m0) + __popc(m1)) * 4 <= NPOS)
+        ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, WPW, PWS, FAST, true>(acc, wr, is, m0, m1);
+      else
+        ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, WPW, PWS, FAST, false, NOSKIP>(acc, wr, is, m0,
+                                                                                 m1);
     }
     __syncthreads();
   }

@@ -27,7 +27,10 @@
 // k_data (src/ecr.cpp:79-91) summed as in ecr_spmv_conv (:117-120).
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
+#include "ecr_body.cuh"
 
 namespace sconv_cu {
 
@@ -42,18 +45,19 @@ struct WsCfg {
   static constexpr int PITCH = WPW <= 8 ? 8 : 16;    // sub-patch row pitch (floats)
   static constexpr int PATCH = WPH * PITCH;          // floats per (warp, channel)
   static constexpr int NPOS = WPH * WPW;
-  static constexpr int IN_STAGE = WPC * CC * PATCH;  // floats
+  static constexpr int IN_STAGE = (WPC * CC * PATCH + 31) / 32 * 32;  // floats, 128B aligned
   static constexpr int W_STAGE = CC * KK * KT;       // floats
   static constexpr int STAGE = IN_STAGE + W_STAGE;
   static constexpr int NT = 32 * (WPC + 1);          // + producer warp
-  static constexpr int MINB = NT > 256 ? 1 : (TH * TW * R <= 32 ? 3 : 2);  // CTAs per SM
+  static constexpr int MINB = (NT > 256 || R >= 8) ? 1 : (TH * TW * R <= 32 ? 3 : 2);  // CTAs/SM
   static constexpr int SMEM_BYTES = NS * STAGE * 4 + 2 * NS * 8;
   static constexpr int CELLS = WPC * NPOS;           // input cells per channel
   static constexpr int CELLS_PER_LANE = (CELLS + 31) / 32;
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
   static_assert(R == 2 || R == 4 || R == 8, "R");
   static_assert(P == 0 || (TH % P == 0 && TW % P == 0), "pool tile");
-  static_assert((IN_STAGE * 4) % 16 == 0, "weight region must stay 16B aligned");
+  static_assert((IN_STAGE * 4) % 128 == 0 && (STAGE * 4) % 128 == 0, "TMA destination alignment");
+  static constexpr unsigned W_BYTES = W_STAGE * 4;   // one TMA box (CC x KK x KT floats)
 };
 
 struct WsArgs {
@@ -98,6 +102,22 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
   while (!mbar_try_wait(b, parity)) __nanosleep(256);
 }
 
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+// TMA: one CC x KK x KT box of the transposed filters wt[C][KK][Kp] into the
+// stage's weight region; completion is counted on the stage's `full` barrier.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
 template <int R>
 __device__ __forceinline__ int ws_lane_chan(int lane, int r) {
   if constexpr (R >= 4) {
@@ -133,7 +153,8 @@ __device__ __forceinline__ void ws_lds_w(float (&dst)[R], const float* row, int 
 #endif
 
 template <class Cfg, bool FAST>
-__global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) ecr_ws_kernel(const WsArgs a) {
+__global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
+    ecr_ws_kernel(const WsArgs a, const __grid_constant__ CUtensorMap wmap) {
   constexpr int KH = Cfg::KH, KW = Cfg::KW, S = Cfg::S, TH = Cfg::TH, TW = Cfg::TW, R = Cfg::R;
   constexpr int KK = Cfg::KK, KT = Cfg::KT, CC = Cfg::CC, NS = Cfg::NS, P = Cfg::P;
   constexpr int WPC = Cfg::WPC, WPH = Cfg::WPH, WPW = Cfg::WPW, PITCH = Cfg::PITCH;
@@ -157,7 +178,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) ecr_ws_kernel(const WsArgs
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 32);
+      mbar_init(&full[s], 33);  // 32 cp.async lane arrivals + the TMA expect_tx arrival
       mbar_init(&empty[s], WPC);
     }
   }
@@ -182,7 +203,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) ecr_ws_kernel(const WsArgs
       src_off[e] = ok[e] ? static_cast<int>((static_cast<size_t>(n) * C * H + iy) * W + ix) : 0;
       dst_off[e] = (wi * CC) * PATCH + Y * PITCH + X;
     }
-    constexpr int QW = KT / 4;  // 16B pieces per weight row
+    if (lane == 0)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
     for (int k = 0; k < nchunks; ++k) {
       const int s = k % NS;
       if (k >= NS) mbar_wait_sleep(&empty[s], ((k / NS) + 1) & 1);
@@ -200,13 +222,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) ecr_ws_kernel(const WsArgs
           }
         }
       }
-      for (int idx = lane; idx < CC * KK * QW; idx += 32) {
-        const int row = idx / QW, q = idx - row * QW;
-        const int ch = row / KK;
-        const bool v = c0 + ch < C && k0 + 4 * q < a.Kp;
-        const float* src =
-            v ? a.wt + (static_cast<size_t>(c0) * KK + row) * a.Kp + k0 + 4 * q : a.wt;
-        cp_async16(w_s + row * KT + 4 * q, src, v);
+      if (lane == 0) {  // weights: one TMA box, zero-filled past C and Kp
+        mbar_arrive_expect_tx(&full[s], Cfg::W_BYTES);
+        tma_load_3d(w_s, &wmap, k0, 0, c0, &full[s]);
       }
       mbar_arrive_cp_async(&full[s]);
     }
@@ -250,52 +268,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) ecr_ws_kernel(const WsArgs
 #pragma unroll
         for (int ij = 0; ij < KK; ++ij) ws_lds_w<R>(wr[ij], wsrc + ij * KT, lane);
 
-#pragma unroll
-        for (int Y = 0; Y < WPH; ++Y) {
-          constexpr int W4 = (WPW + 3) / 4;
-          float row[4 * W4];
-#pragma unroll
-          for (int q = 0; q < W4; ++q) {
-            const float4 v4 = *reinterpret_cast<const float4*>(ic + Y * PITCH + 4 * q);
-            row[4 * q + 0] = v4.x;
-            row[4 * q + 1] = v4.y;
-            row[4 * q + 2] = v4.z;
-            row[4 * q + 3] = v4.w;
-          }
-#pragma unroll
-          for (int X = 0; X < WPW; ++X) {
-            const int b = Y * PITCH + X;
-            const bool nz = b < 32 ? ((m0 >> b) & 1u) : ((m1 >> (b - 32)) & 1u);
-            if (nz) {  // warp-uniform: the mask came from a ballot
-#if SCONV_WS_GUARD == 1
-              SCONV_KEEP_BRANCH();
-#elif SCONV_WS_GUARD == 2
-              __syncwarp();
-#endif
-              const float v = row[X];
-#pragma unroll
-              for (int i = 0; i < KH; ++i) {
-                const int dy = Y - i;
-                if (dy < 0 || dy % S != 0 || dy / S >= TH) continue;
-#pragma unroll
-                for (int j = 0; j < KW; ++j) {
-                  const int dx = X - j;
-                  if (dx < 0 || dx % S != 0 || dx / S >= TW) continue;
-                  if constexpr (FAST) {
-#pragma unroll
-                    for (int r = 0; r < R; r += 2)
-                      ffma2(acc[dy / S][dx / S][r], acc[dy / S][dx / S][r + 1], wr[i * KW + j][r],
-                            wr[i * KW + j][r + 1], v);
-                  } else {
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                      acc[dy / S][dx / S][r] = mac<false>(acc[dy / S][dx / S][r], v, wr[i * KW + j][r]);
-                  }
-                }
-              }
-            }
-          }
-        }
+        if ((__popc(m0) + __popc(m1)) * 4 <= Cfg::NPOS)
+          ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, true>(acc, wr, ic, m0, m1);
+        else
+          ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, false>(acc, wr, ic, m0,
+                                                                                m1);
       }
     }
     __syncwarp();

@@ -262,6 +262,43 @@ template <int P> using WsA = WsCfg<3, 3, 1, 4, 4, 4, 7, 4, 4, P>;  // K >= 128
 template <int P> using WsB = WsCfg<3, 3, 1, 2, 7, 4, 7, 4, 4, P>;  // 14-wide maps, K >= 128
 template <int P> using WsC = WsCfg<3, 3, 1, 4, 6, 2, 7, 4, 4, P>;  // K = 64
 template <int P> using WsD = WsCfg<3, 3, 1, 2, 4, 4, 7, 4, 3, P>;  // small tiles, 3 CTAs/SM
+template <int P> using WsE = WsCfg<3, 3, 1, 4, 4, 8, 7, 4, 3, P>;  // R = 8, 1 CTA/SM
+template <int P> using WsF = WsCfg<3, 3, 1, 2, 4, 8, 11, 4, 3, P>; // R = 8, 2x4 tiles
+template <int P> using WsG = WsCfg<3, 3, 1, 6, 6, 2, 7, 4, 4, P>;  // K = 64, 6x6 tiles
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// Tensor map over the transposed filters wt[C][KK][Kp] (fp32), box KT x KK x CC.
+int weight_map(sconv_cu_ctx* ctx, const float* wt, int C, int KK, int Kp, int KT, int CC,
+               CUtensorMap* map) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return fail(ctx, SCONV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {cuuint64_t(Kp), cuuint64_t(KK), cuuint64_t(C)};
+  const cuuint64_t strides[2] = {cuuint64_t(Kp) * 4, cuuint64_t(KK) * Kp * 4};
+  const cuuint32_t box[3] = {cuuint32_t(KT), cuuint32_t(KK), cuuint32_t(CC)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(wt), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, SCONV_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return SCONV_OK;
+}
 
 template <class Cfg, bool FAST>
 int launch_ws_cfg(sconv_cu_ctx* ctx, const WsArgs& a0) {
@@ -277,26 +314,28 @@ int launch_ws_cfg(sconv_cu_ctx* ctx, const WsArgs& a0) {
   a.tiles_per_img = a.tiles_x * ((a.OH + Cfg::TH - 1) / Cfg::TH);
   a.total_tiles = a.tiles_per_img * a.N;
   dim3 grid((a.total_tiles + Cfg::WPC - 1) / Cfg::WPC, (a.K + Cfg::KT - 1) / Cfg::KT);
-  kern<<<grid, Cfg::NT, Cfg::SMEM_BYTES, ctx->stream>>>(a);
+  CUtensorMap wmap;
+  TRY(weight_map(ctx, a.wt, a.C, Cfg::KK, a.Kp, Cfg::KT, Cfg::CC, &wmap));
+  kern<<<grid, Cfg::NT, Cfg::SMEM_BYTES, ctx->stream>>>(a, wmap);
   return finish_launch(ctx, "ecr_ws_kernel");
 }
 
 // which ws config (0 = none); P is 0 (ECR) or 2 (PECR 2x2/2)
-int pick_ws(int K, int OW, int kh, int kw, int S, int P) {
+int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P) {
   if (!(kh == 3 && kw == 3 && S == 1 && (P == 0 || P == 2) && K >= 32)) return 0;
   const char* e = std::getenv("SCONV_KERNEL");
   if (e && std::strcmp(e, "v2") == 0) return 0;
-  if (e && e[0] == 'w' && e[1] >= 'A' && e[1] <= 'D') return e[1] - 'A' + 1;
+  if (e && e[0] == 'w' && e[1] >= 'A' && e[1] <= 'G') return e[1] - 'A' + 1;
   if (e && std::strcmp(e, "v3") == 0) {
     if (K <= 64) return 3;
     if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
     return 1;
   }
-  // Measured on B200 (tools/tune.py, profiles/r01): v3 wins on the K = 512
-  // layers (conv4_x / conv5_x: 5-6% faster, no partial tiles), v2 on the
-  // shallower ones, where v3's per-CTA producer pipeline start-up is not
-  // amortised over enough channel chunks.
-  if (K < 512) return 0;
+  // Measured on B200 (tools/tune.py, profiles/r01): with the filters staged
+  // by TMA, v3 beats v2 on every K >= 128 VGG layer (17-20%); for K = 64 the
+  // 6x6-tile WsG wins at sparsity 0.7 (5%) once there are enough channel
+  // chunks to fill the producer pipeline (conv1_1's C = 3 stays on v2).
+  if (K < 128) return C >= 16 ? 7 : 0;
   if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
   return 1;
 }
@@ -307,6 +346,9 @@ int launch_ws(sconv_cu_ctx* ctx, int which, int P, const WsArgs& a) {
     case 1: return P ? launch_ws_cfg<WsA<2>, FAST>(ctx, a) : launch_ws_cfg<WsA<0>, FAST>(ctx, a);
     case 2: return launch_ws_cfg<WsB<0>, FAST>(ctx, a);
     case 4: return P ? launch_ws_cfg<WsD<2>, FAST>(ctx, a) : launch_ws_cfg<WsD<0>, FAST>(ctx, a);
+    case 5: return P ? launch_ws_cfg<WsE<2>, FAST>(ctx, a) : launch_ws_cfg<WsE<0>, FAST>(ctx, a);
+    case 6: return P ? launch_ws_cfg<WsF<2>, FAST>(ctx, a) : launch_ws_cfg<WsF<0>, FAST>(ctx, a);
+    case 7: return P ? launch_ws_cfg<WsG<2>, FAST>(ctx, a) : launch_ws_cfg<WsG<0>, FAST>(ctx, a);
     default: return P ? launch_ws_cfg<WsC<2>, FAST>(ctx, a) : launch_ws_cfg<WsC<0>, FAST>(ctx, a);
   }
 }
@@ -355,7 +397,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   int P = 0;
   if (pecr && pw == ph && pw == ps) P = pw;
   const int Pk = pecr ? (P ? P : -1) : 0;
-  int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, OW, kh, kw, stride, Pk);
+  int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk);
   int which = (flags & SCONV_F_GENERIC) || ws ? 0 : pick_tiled(k, kh, kw, stride, Pk);
   const int forced = (flags >> 8) & 0xff;
   const bool tileable = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
@@ -363,7 +405,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     if (forced >= 1 && forced <= kNumCfgs) {
       which = forced;
       ws = 0;
-    } else if (forced >= 'A' && forced <= 'D' && !(forced == 'B' && Pk != 0)) {
+    } else if (forced >= 'A' && forced <= 'G' && !(forced == 'B' && Pk != 0)) {
       ws = forced - 'A' + 1;
       which = 0;
     } else {
@@ -606,13 +648,16 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
     TRY(pack_count(nullptr, h, kh, stride, pool_h, pool_stride, &PHo));
     P = (pool_w == pool_h && pool_w == pool_stride) ? pool_w : -1;
   }
-  const int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, OW, kh, kw, stride, P);
+  const int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, c, OW, kh, kw, stride, P);
   const int which = (flags & SCONV_F_GENERIC) || ws ? 0 : pick_tiled(k, kh, kw, stride, P);
   if (ws) {
     switch (ws) {
       case 1: plan_ws<WsA<0>>(out, ws, n, k, OH, OW); break;
       case 2: plan_ws<WsB<0>>(out, ws, n, k, OH, OW); break;
       case 4: plan_ws<WsD<0>>(out, ws, n, k, OH, OW); break;
+      case 5: plan_ws<WsE<0>>(out, ws, n, k, OH, OW); break;
+      case 6: plan_ws<WsF<0>>(out, ws, n, k, OH, OW); break;
+      case 7: plan_ws<WsG<0>>(out, ws, n, k, OH, OW); break;
       default: plan_ws<WsC<0>>(out, ws, n, k, OH, OW); break;
     }
   } else if (which) {

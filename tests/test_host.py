@@ -109,12 +109,13 @@ def test_shard_partition(sc):
 
 
 def test_launch_plan(sc):
-    # K < 512: v2 tiled kernel (Cfg2 for K % 128 == 0, Cfg4 otherwise)
-    p = sc.launch_plan(64, 256, 58, 58, 256, 3, 3, 1)
-    assert p["kernel"] == 2 and p["grid_z"] == 64 and p["grid_y"] == 2 and p["block_threads"] == 256
+    # few input channels: v2 tiled kernel (Cfg4 for K % 128 != 0)
+    p = sc.launch_plan(64, 3, 226, 226, 64, 3, 3, 1)
+    assert p["kernel"] == 4 and p["grid_z"] == 64 and p["block_threads"] == 128
+    # K = 64: v3 with 6x6 tiles (WsG)
     p = sc.launch_plan(64, 64, 226, 226, 64, 3, 3, 1, sc.PoolConfig(2, 2, 2))
-    assert p["kernel"] == 4 and p["smem_bytes"] <= 227 * 1024
-    # K = 512: v3 warp-specialised kernel, 7 consumer warps (4x4 tiles) + 1 producer
+    assert p["kernel"] == 107 and p["smem_bytes"] <= 227 * 1024
+    # K >= 128: v3 warp-specialised kernel, 7 consumer warps (4x4 tiles) + 1 producer
     p = sc.launch_plan(64, 512, 30, 30, 512, 3, 3, 1)
     assert p["kernel"] == 101 and p["grid_y"] == 4 and p["block_threads"] == 256
     assert p["grid_x"] == 64 * 7 * 7 // 7 and p["grid_z"] == 1
