@@ -25,6 +25,11 @@
 
 #include "common.cuh"
 
+// 0: let ptxas if-convert small blocks; 2: keep every block behind its branch
+#ifndef SCONV_BODY_GUARD
+#define SCONV_BODY_GUARD 0
+#endif
+
 namespace sconv_cu {
 
 template <int KH, int KW, int S, int TH, int TW, int R, int WPH, int WPW, int BPITCH, int SPITCH,
@@ -53,6 +58,11 @@ __device__ __forceinline__ void ecr_channel(float (&acc)[TH][TW][R], const float
       const int b = Y * BPITCH + X;
       const bool nz = b < 32 ? ((m0 >> b) & 1u) : ((m1 >> (b - 32)) & 1u);
       if (NOSKIP || nz) {  // warp-uniform
+#if SCONV_BODY_GUARD == 1
+        if constexpr (!NOSKIP) SCONV_KEEP_BRANCH();
+#elif SCONV_BODY_GUARD == 2
+        if constexpr (!NOSKIP) __syncwarp();
+#endif
         const float v = row[X];
 #pragma unroll
         for (int i = 0; i < KH; ++i) {
