@@ -15,7 +15,7 @@ def tm(fn, reps=5):
     e.record(); torch.cuda.synchronize()
     return s.elapsed_time(e) / reps * 1000
 out = {}
-for name, C, K, Ho in [("conv1_2",64,64,224),("conv2_2",128,128,112),("conv3_2",256,256,56),("conv4_2",512,512,28),("conv5_1",512,512,14)]:
+for name, C, K, Ho in [("conv1_1",3,64,224),("conv1_2",64,64,224),("conv2_2",128,128,112),("conv3_2",256,256,56),("conv4_2",512,512,28),("conv5_1",512,512,14)]:
     g = torch.Generator(device=dev); g.manual_seed(1)
     x = torch.rand(N, C, Ho + 2, Ho + 2, device=dev, generator=g)
     x = x * (torch.rand(x.shape, device=dev, generator=g) >= S)
