@@ -239,6 +239,25 @@ def test_forced_kernels(sc, orc, shape, kid):
         assert close(sc.pecr_conv_pool_batched(x, f, 1, pool, fast=True, kernel=kid), pref)
 
 
+@pytest.mark.parametrize("n", [8, 9, 35])
+def test_host_pointer_pipeline(sc, orc, n):
+    """Host-pointer calls with n >= 8 run as image chunks alternating between
+    two streams (H2D / compute / D2H overlap); results, counters and the
+    ragged last chunk must match the oracle exactly."""
+    c, h, w, k = 5, 12, 14, 64
+    x, f = inputs(orc, n, c, h, w, k, 3, 3, 0.7, seed=4242 + n)
+    ops = sc.OpCount()
+    y = sc.ecr_conv_batched(x, f, 1, counters=ops)
+    ref, rops = orc.ecr_conv(x, f, 1)
+    assert bits_equal(y, ref)
+    assert (ops.multiplications, ops.additions) == rops
+    ops = sc.OpCount()
+    p = sc.pecr_conv_pool_batched(x, f, 1, sc.PoolConfig(2, 2, 2), counters=ops)
+    pref, pops = orc.pecr_conv(x, f, 1, 2, 2, 2, 0)
+    assert bits_equal(p, pref)
+    assert (ops.multiplications, ops.additions) == pops
+
+
 def test_errors(sc):
     x = np.ones((1, 2, 5, 5), np.float32)
     with pytest.raises(sc.ShapeError):
