@@ -1,0 +1,63 @@
+// internal.h -- declarations shared by the translation units of
+// libsconv_cuda.so (not part of the C ABI): the context object, the error
+// helpers, and the v2 / v3 kernel registries (reg_v2.cu, reg_v3_*.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "kernels/ecr_tiled.cuh"
+#include "kernels/ecr_ws.cuh"
+#include "sconv_cuda.h"
+
+struct sconv_cu_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+  char* ws = nullptr;
+  size_t ws_cap = 0;
+  int num_sms = 148;
+  int smem_optin = 0;
+  cudaStream_t aux = nullptr;       // second stream of the chunked host-pointer pipeline
+  cudaEvent_t ev_w = nullptr, ev_done = nullptr;
+};
+
+namespace sconv_cu {
+namespace host {
+
+int fail(sconv_cu_ctx* ctx, int code, const char* fmt, ...);
+int finish_launch(sconv_cu_ctx* ctx, const char* what);
+unsigned grid_for(size_t work, int threads, int num_sms);
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, SCONV_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+#define TRY(expr)                 \
+  do {                            \
+    const int rc_ = (expr);       \
+    if (rc_ != SCONV_OK) return rc_; \
+  } while (0)
+
+// v2 tiled registry (reg_v2.cu): config id for a shape (0 = generic), launch, plan.
+constexpr int kNumCfgs = 7;
+int pick_tiled(int K, int kh, int kw, int S, int P);
+int launch_tiled(sconv_cu_ctx* ctx, bool fast, int which, int P, const TiledArgs& a, int N);
+void plan_for(sconv_launch_plan* p, int which, int N, int K, int OH, int OW);
+
+// v3 warp-specialised registry (reg_v3.cu / reg_v3_exact.cu / reg_v3_fast.cu).
+int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P);
+int launch_ws_fast(sconv_cu_ctx* ctx, int which, int P, const WsArgs& a);
+int launch_ws_exact(sconv_cu_ctx* ctx, int which, int P, const WsArgs& a);
+void plan_ws(sconv_launch_plan* p, int which, int N, int K, int OH, int OW);
+
+}  // namespace host
+}  // namespace sconv_cu

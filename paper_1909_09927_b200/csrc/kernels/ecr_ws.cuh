@@ -171,7 +171,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
   // masks land in vector registers and every zero-skip branch pays a vector
   // bit test right before it (plus BRA.DIV checks for the guard).
   const int warp = __shfl_sync(kFull, tid >> 5, 0), lane = tid & 31;
-  const int k0 = blockIdx.y * KT;
+  // K-blocks vary fastest over the linear grid, so the CTAs that read the same
+  // input patches run together and the patch is fetched from HBM once.
+  const int kblocks = (a.K + KT - 1) / KT;
+  const int cta = blockIdx.x / kblocks;
+  const int k0 = (blockIdx.x - cta * kblocks) * KT;
   const int C = a.C, H = a.H, W = a.W, K = a.K;
   const int nchunks = (C + CC - 1) / CC;
 
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
       const int q = lane + 32 * e;
       const int wi = q / Cfg::NPOS, pos = q - (q / Cfg::NPOS) * Cfg::NPOS;
       const int Y = pos / WPW, X = pos - (pos / WPW) * WPW;
-      const int t = blockIdx.x * WPC + wi;
+      const int t = cta * WPC + wi;
       const int n = t / a.tiles_per_img, tt = t - n * a.tiles_per_img;
       const int ty = tt / a.tiles_x, tx = tt - ty * a.tiles_x;
       const int iy = ty * TH * S + Y, ix = tx * TW * S + X;
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
   }
 
   // ------------------------------- consumers -------------------------------
-  const int t = blockIdx.x * WPC + warp;
+  const int t = cta * WPC + warp;
   const bool active = t < a.total_tiles;
   const int n = active ? t / a.tiles_per_img : 0;
   const int tt = t - n * a.tiles_per_img;

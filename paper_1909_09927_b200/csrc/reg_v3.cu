@@ -1,0 +1,59 @@
+// reg_v3.cu -- v3 selection and launch plans (no kernel instantiations).
+#include "reg_v3.inc"
+
+namespace sconv_cu {
+namespace host {
+
+// which ws config (0 = none); P is 0 (ECR) or 2 (PECR 2x2/2)
+int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P) {
+  if (!(kh == 3 && kw == 3 && S == 1 && (P == 0 || P == 2) && K >= 32)) return 0;
+  const char* e = std::getenv("SCONV_KERNEL");
+  if (e && std::strcmp(e, "v2") == 0) return 0;
+  if (e && e[0] == 'w' && e[1] >= 'A' && e[1] <= 'G') return e[1] - 'A' + 1;
+  if (e && std::strcmp(e, "v3") == 0) {
+    if (K <= 64) return 3;
+    if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
+    return 1;
+  }
+  // Measured on B200 (tools/tune.py, profiles/r01): with the filters staged
+  // by TMA, v3 beats v2 on every K >= 128 VGG layer (17-20%); for K = 64 the
+  // 6x6-tile WsG wins at sparsity 0.7 (5%) once there are enough channel
+  // chunks to fill the producer pipeline (conv1_1's C = 3 stays on v2).
+  if (K < 128) return C >= 16 ? 7 : 0;
+  if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
+  return 1;
+}
+
+// Plan of a v3 launch: kernel id 100 + registry index; grid_x counts CTAs of
+// WPC warp tiles over the flat (image, tile) list, grid_z is 1.
+namespace {
+template <class Cfg>
+void plan_ws_t(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
+  const long tiles = long((OH + Cfg::TH - 1) / Cfg::TH) * ((OW + Cfg::TW - 1) / Cfg::TW) * N;
+  p->kernel = 100 + which;
+  p->grid_x = static_cast<int>((tiles + Cfg::WPC - 1) / Cfg::WPC) * ((K + Cfg::KT - 1) / Cfg::KT);
+  p->grid_y = 1;
+  p->grid_z = 1;
+  p->block_threads = Cfg::NT;
+  p->smem_bytes = Cfg::SMEM_BYTES;
+  p->tile_h = Cfg::TH;
+  p->tile_w = Cfg::TW;
+  p->tile_k = Cfg::KT;
+}
+
+}  // namespace
+
+void plan_ws(sconv_launch_plan* out, int ws, int n, int k, int OH, int OW) {
+  switch (ws) {
+    case 1: plan_ws_t<WsA<0>>(out, ws, n, k, OH, OW); break;
+    case 2: plan_ws_t<WsB<0>>(out, ws, n, k, OH, OW); break;
+    case 4: plan_ws_t<WsD<0>>(out, ws, n, k, OH, OW); break;
+    case 5: plan_ws_t<WsE<0>>(out, ws, n, k, OH, OW); break;
+    case 6: plan_ws_t<WsF<0>>(out, ws, n, k, OH, OW); break;
+    case 7: plan_ws_t<WsG<0>>(out, ws, n, k, OH, OW); break;
+    default: plan_ws_t<WsC<0>>(out, ws, n, k, OH, OW); break;
+  }
+}
+
+}  // namespace host
+}  // namespace sconv_cu

@@ -17,29 +17,15 @@
 #include <thread>
 #include <vector>
 
-#include "kernels/ecr_tiled.cuh"
-#include "kernels/ecr_ws.cuh"
+#include "host/internal.h"
 #include "kernels/format.cuh"
 #include "kernels/generic.cuh"
-#include "sconv_cuda.h"
 
 using namespace sconv_cu;
+using namespace sconv_cu::host;
 
-struct sconv_cu_ctx {
-  int device = 0;
-  cudaStream_t own = nullptr;
-  cudaStream_t stream = nullptr;
-  std::string err;
-  uint64_t launches = 0;
-  char* ws = nullptr;
-  size_t ws_cap = 0;
-  int num_sms = 148;
-  int smem_optin = 0;
-  cudaStream_t aux = nullptr;       // second stream of the chunked host-pointer pipeline
-  cudaEvent_t ev_w = nullptr, ev_done = nullptr;
-};
-
-namespace {
+namespace sconv_cu {
+namespace host {
 
 thread_local std::string g_noctx_err;
 
@@ -53,19 +39,23 @@ int fail(sconv_cu_ctx* ctx, int code, const char* fmt, ...) {
   return code;
 }
 
-#define CK(expr)                                                                          \
-  do {                                                                                    \
-    cudaError_t e_ = (expr);                                                              \
-    if (e_ != cudaSuccess)                                                                \
-      return fail(ctx, SCONV_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
-                  __FILE__, __LINE__);                                                    \
-  } while (0)
+unsigned grid_for(size_t work, int threads, int num_sms) {
+  const size_t blocks = (work + threads - 1) / threads;
+  return static_cast<unsigned>(std::min<size_t>(std::max<size_t>(blocks, 1), size_t(num_sms) * 64));
+}
 
-#define TRY(expr)                 \
-  do {                            \
-    const int rc_ = (expr);       \
-    if (rc_ != SCONV_OK) return rc_; \
-  } while (0)
+int finish_launch(sconv_cu_ctx* ctx, const char* what) {
+  ctx->launches++;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, SCONV_ERR_CUDA, "launch %s: %s", what, cudaGetErrorString(e));
+  return SCONV_OK;
+}
+
+}  // namespace host
+}  // namespace sconv_cu
+
+
+namespace {
 
 struct DeviceGuard {
   int prev = -1;
@@ -137,240 +127,6 @@ int pack_count(sconv_cu_ctx* ctx, int in, int k, int cs, int p, int ps, int* out
   return SCONV_OK;
 }
 
-unsigned grid_for(size_t work, int threads, int num_sms) {
-  const size_t blocks = (work + threads - 1) / threads;
-  return static_cast<unsigned>(std::min<size_t>(std::max<size_t>(blocks, 1), size_t(num_sms) * 64));
-}
-
-int finish_launch(sconv_cu_ctx* ctx, const char* what) {
-  ctx->launches++;
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(ctx, SCONV_ERR_CUDA, "launch %s: %s", what, cudaGetErrorString(e));
-  return SCONV_OK;
-}
-
-// ---------------------------------------------------------------------------
-// Tiled kernel registry.  Specialisations exist for the VGG / AlexNet /
-// GoogLeNet 3x3 stride-1 shapes; every other shape takes the generic kernel.
-// ---------------------------------------------------------------------------
-// TiledCfg<KH, KW, S, TH, TW, R, WK, WSY, WSX, CC, P> -- warp tile TH x TW
-// outputs x 32R channels, CTA = WSY x WSX warps (x WK along channels).
-template <int P> using Cfg1 = TiledCfg<3, 3, 1, 4, 4, 8, 1, 2, 4, 8, P>;  // 8x16 x 256ch
-template <int P> using Cfg2 = TiledCfg<3, 3, 1, 4, 4, 4, 1, 2, 4, 8, P>;  // 8x16 x 128ch
-template <int P> using Cfg3 = TiledCfg<3, 3, 1, 4, 8, 4, 1, 2, 2, 8, P>;  // 8x16 x 128ch
-template <int P> using Cfg4 = TiledCfg<3, 3, 1, 4, 8, 2, 1, 2, 2, 8, P>;  // 8x16 x 64ch
-template <int P> using Cfg5 = TiledCfg<3, 3, 1, 2, 8, 8, 1, 4, 2, 8, P>;  // 8x16 x 256ch
-template <int P> using Cfg6 = TiledCfg<3, 3, 1, 4, 4, 2, 1, 2, 4, 8, P>;  // 8x16 x 64ch
-template <int P> using Cfg7 = TiledCfg<3, 3, 1, 2, 4, 4, 1, 4, 2, 8, P>;  // 8x8 x 128ch
-constexpr int kNumCfgs = 7;
-
-template <class Cfg>
-constexpr int min_blocks() {
-  return Cfg::R >= 8 ? 1 : 2;
-}
-
-template <class Cfg, bool FAST, bool NOSKIP = false>
-int launch_tiled_cfg(sconv_cu_ctx* ctx, const TiledArgs& a, int N) {
-  auto kern = ecr_tiled_kernel<Cfg, FAST, min_blocks<Cfg>(), NOSKIP>;
-  static bool attr_done[64] = {};
-  const int slot = ctx->device & 63;
-  if (!attr_done[slot]) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_done[slot] = true;
-  }
-  const int tiles_y = (a.OH + Cfg::OTH - 1) / Cfg::OTH;
-  const int tiles_x = (a.OW + Cfg::OTW - 1) / Cfg::OTW;
-  TiledArgs b = a;
-  b.tiles_x = tiles_x;
-  dim3 grid(tiles_y * tiles_x, (a.K + Cfg::KT - 1) / Cfg::KT, N);
-  kern<<<grid, Cfg::NT, Cfg::SMEM_BYTES, ctx->stream>>>(b);
-  return finish_launch(ctx, "ecr_tiled_kernel");
-}
-
-int forced_cfg() {
-  static const int v = [] {
-    const char* e = std::getenv("SCONV_TILED_CFG");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
-// which tiled config (0 = none -> generic)
-int pick_tiled(int K, int kh, int kw, int S, int P) {
-  if (!(kh == 3 && kw == 3 && S == 1 && (P == 0 || P == 2) && K >= 32)) return 0;
-  const int f = forced_cfg();
-  if ((f >= 1 && f <= kNumCfgs) || (f >= 11 && f <= 17 && P == 0)) return f;
-  if (K % 128 == 0) return 2;  // measured best on VGG K=128..512 (tools/tune.py)
-  return 4;
-}
-
-template <template <int> class CfgT, bool FAST>
-int launch_p(sconv_cu_ctx* ctx, int P, const TiledArgs& a, int N) {
-  return P == 0 ? launch_tiled_cfg<CfgT<0>, FAST>(ctx, a, N)
-                : launch_tiled_cfg<CfgT<2>, FAST>(ctx, a, N);
-}
-
-template <bool FAST>
-int launch_tiled(sconv_cu_ctx* ctx, int which, int P, const TiledArgs& a, int N) {
-  switch (which) {
-    case 1: return launch_p<Cfg1, FAST>(ctx, P, a, N);
-    case 2: return launch_p<Cfg2, FAST>(ctx, P, a, N);
-    case 3: return launch_p<Cfg3, FAST>(ctx, P, a, N);
-    case 4: return launch_p<Cfg4, FAST>(ctx, P, a, N);
-    case 5: return launch_p<Cfg5, FAST>(ctx, P, a, N);
-    case 6: return launch_p<Cfg6, FAST>(ctx, P, a, N);
-    case 17: return launch_tiled_cfg<Cfg7<0>, FAST, true>(ctx, a, N);  // calibration
-    case 11: return launch_tiled_cfg<Cfg1<0>, FAST, true>(ctx, a, N);  // calibration
-    case 12: return launch_tiled_cfg<Cfg2<0>, FAST, true>(ctx, a, N);  // calibration
-    default: return launch_p<Cfg7, FAST>(ctx, P, a, N);
-  }
-}
-
-template <class Cfg>
-void fill_plan(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
-  p->kernel = which;
-  p->grid_x = ((OH + Cfg::OTH - 1) / Cfg::OTH) * ((OW + Cfg::OTW - 1) / Cfg::OTW);
-  p->grid_y = (K + Cfg::KT - 1) / Cfg::KT;
-  p->grid_z = N;
-  p->block_threads = Cfg::NT;
-  p->smem_bytes = Cfg::SMEM_BYTES;
-  p->tile_h = Cfg::OTH;
-  p->tile_w = Cfg::OTW;
-  p->tile_k = Cfg::KT;
-}
-
-void plan_for(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
-  switch (which) {
-    case 1: return fill_plan<Cfg1<0>>(p, which, N, K, OH, OW);
-    case 2: return fill_plan<Cfg2<0>>(p, which, N, K, OH, OW);
-    case 3: return fill_plan<Cfg3<0>>(p, which, N, K, OH, OW);
-    case 4: return fill_plan<Cfg4<0>>(p, which, N, K, OH, OW);
-    case 5: return fill_plan<Cfg5<0>>(p, which, N, K, OH, OW);
-    case 11: return fill_plan<Cfg1<0>>(p, which, N, K, OH, OW);
-    case 12: return fill_plan<Cfg2<0>>(p, which, N, K, OH, OW);
-    case 6: return fill_plan<Cfg6<0>>(p, which, N, K, OH, OW);
-    case 17: return fill_plan<Cfg7<0>>(p, which, N, K, OH, OW);
-    default: return fill_plan<Cfg7<0>>(p, which, N, K, OH, OW);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// v3 warp-specialised kernel registry (kernels/ecr_ws.cuh).  WsCfg<KH, KW, S,
-// TH, TW, R, WPC, CC, NS, P>: warp tile TH x TW outputs x 32R channels, WPC
-// consumer warps + 1 producer warp, CC channels per stage, NS stages.
-// ---------------------------------------------------------------------------
-// 7 consumer warps + the producer = 8 warps, two CTAs per SM.
-template <int P> using WsA = WsCfg<3, 3, 1, 4, 4, 4, 7, 4, 4, P>;  // K >= 128
-template <int P> using WsB = WsCfg<3, 3, 1, 2, 7, 4, 7, 4, 4, P>;  // 14-wide maps, K >= 128
-template <int P> using WsC = WsCfg<3, 3, 1, 4, 6, 2, 7, 4, 4, P>;  // K = 64
-template <int P> using WsD = WsCfg<3, 3, 1, 2, 4, 4, 7, 4, 3, P>;  // small tiles, 3 CTAs/SM
-template <int P> using WsE = WsCfg<3, 3, 1, 4, 4, 8, 7, 4, 3, P>;  // R = 8, 1 CTA/SM
-template <int P> using WsF = WsCfg<3, 3, 1, 2, 4, 8, 11, 4, 3, P>; // R = 8, 2x4 tiles
-template <int P> using WsG = WsCfg<3, 3, 1, 6, 6, 2, 7, 4, 4, P>;  // K = 64, 6x6 tiles
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return static_cast<EncodeTiledFn>(nullptr);
-    return reinterpret_cast<EncodeTiledFn>(p);
-  }();
-  return fn;
-}
-
-// Tensor map over the transposed filters wt[C][KK][Kp] (fp32), box KT x KK x CC.
-int weight_map(sconv_cu_ctx* ctx, const float* wt, int C, int KK, int Kp, int KT, int CC,
-               CUtensorMap* map) {
-  EncodeTiledFn enc = encode_tiled();
-  if (!enc) return fail(ctx, SCONV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[3] = {cuuint64_t(Kp), cuuint64_t(KK), cuuint64_t(C)};
-  const cuuint64_t strides[2] = {cuuint64_t(Kp) * 4, cuuint64_t(KK) * Kp * 4};
-  const cuuint32_t box[3] = {cuuint32_t(KT), cuuint32_t(KK), cuuint32_t(CC)};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(wt), dims,
-                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(ctx, SCONV_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
-  return SCONV_OK;
-}
-
-template <class Cfg, bool FAST>
-int launch_ws_cfg(sconv_cu_ctx* ctx, const WsArgs& a0) {
-  auto kern = ecr_ws_kernel<Cfg, FAST>;
-  static bool attr_done[64] = {};
-  const int slot = ctx->device & 63;
-  if (!attr_done[slot]) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_done[slot] = true;
-  }
-  WsArgs a = a0;
-  a.tiles_x = (a.OW + Cfg::TW - 1) / Cfg::TW;
-  a.tiles_per_img = a.tiles_x * ((a.OH + Cfg::TH - 1) / Cfg::TH);
-  a.total_tiles = a.tiles_per_img * a.N;
-  dim3 grid((a.total_tiles + Cfg::WPC - 1) / Cfg::WPC, (a.K + Cfg::KT - 1) / Cfg::KT);
-  CUtensorMap wmap;
-  TRY(weight_map(ctx, a.wt, a.C, Cfg::KK, a.Kp, Cfg::KT, Cfg::CC, &wmap));
-  kern<<<grid, Cfg::NT, Cfg::SMEM_BYTES, ctx->stream>>>(a, wmap);
-  return finish_launch(ctx, "ecr_ws_kernel");
-}
-
-// which ws config (0 = none); P is 0 (ECR) or 2 (PECR 2x2/2)
-int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P) {
-  if (!(kh == 3 && kw == 3 && S == 1 && (P == 0 || P == 2) && K >= 32)) return 0;
-  const char* e = std::getenv("SCONV_KERNEL");
-  if (e && std::strcmp(e, "v2") == 0) return 0;
-  if (e && e[0] == 'w' && e[1] >= 'A' && e[1] <= 'G') return e[1] - 'A' + 1;
-  if (e && std::strcmp(e, "v3") == 0) {
-    if (K <= 64) return 3;
-    if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
-    return 1;
-  }
-  // Measured on B200 (tools/tune.py, profiles/r01): with the filters staged
-  // by TMA, v3 beats v2 on every K >= 128 VGG layer (17-20%); for K = 64 the
-  // 6x6-tile WsG wins at sparsity 0.7 (5%) once there are enough channel
-  // chunks to fill the producer pipeline (conv1_1's C = 3 stays on v2).
-  if (K < 128) return C >= 16 ? 7 : 0;
-  if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
-  return 1;
-}
-
-template <bool FAST>
-int launch_ws(sconv_cu_ctx* ctx, int which, int P, const WsArgs& a) {
-  switch (which) {
-    case 1: return P ? launch_ws_cfg<WsA<2>, FAST>(ctx, a) : launch_ws_cfg<WsA<0>, FAST>(ctx, a);
-    case 2: return launch_ws_cfg<WsB<0>, FAST>(ctx, a);
-    case 4: return P ? launch_ws_cfg<WsD<2>, FAST>(ctx, a) : launch_ws_cfg<WsD<0>, FAST>(ctx, a);
-    case 5: return P ? launch_ws_cfg<WsE<2>, FAST>(ctx, a) : launch_ws_cfg<WsE<0>, FAST>(ctx, a);
-    case 6: return P ? launch_ws_cfg<WsF<2>, FAST>(ctx, a) : launch_ws_cfg<WsF<0>, FAST>(ctx, a);
-    case 7: return P ? launch_ws_cfg<WsG<2>, FAST>(ctx, a) : launch_ws_cfg<WsG<0>, FAST>(ctx, a);
-    default: return P ? launch_ws_cfg<WsC<2>, FAST>(ctx, a) : launch_ws_cfg<WsC<0>, FAST>(ctx, a);
-  }
-}
-
-// Plan of a v3 launch: kernel id 100 + registry index; grid_x counts CTAs of
-// WPC warp tiles over the flat (image, tile) list, grid_z is 1.
-template <class Cfg>
-void plan_ws(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
-  const long tiles = long((OH + Cfg::TH - 1) / Cfg::TH) * ((OW + Cfg::TW - 1) / Cfg::TW) * N;
-  p->kernel = 100 + which;
-  p->grid_x = static_cast<int>((tiles + Cfg::WPC - 1) / Cfg::WPC);
-  p->grid_y = (K + Cfg::KT - 1) / Cfg::KT;
-  p->grid_z = 1;
-  p->block_threads = Cfg::NT;
-  p->smem_bytes = Cfg::SMEM_BYTES;
-  p->tile_h = Cfg::TH;
-  p->tile_w = Cfg::TW;
-  p->tile_k = Cfg::KT;
-}
-
 // Shared body of the fused ECR / PECR entries.
 int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, const float* filt,
                int k, int kh, int kw, int stride, int pw, int ph, int ps, int mode, float* y,
@@ -399,9 +155,9 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   int P = 0;
   if (pecr && pw == ph && pw == ps) P = pw;
   const int Pk = pecr ? (P ? P : -1) : 0;
+  const int forced = (flags >> 8) & 0xff;
   int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk);
   int which = (flags & SCONV_F_GENERIC) || ws ? 0 : pick_tiled(k, kh, kw, stride, Pk);
-  const int forced = (flags >> 8) & 0xff;
   const bool tileable = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
   if (forced && tileable && !(flags & SCONV_F_GENERIC)) {
     if (forced >= 1 && forced <= kNumCfgs) {
@@ -484,10 +240,10 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
                          cudaMemcpyHostToDevice, cs));
     if (ws) {
       WsArgs a{dx, wt, dy, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, mode};
-      TRY(fast ? launch_ws<true>(ctx, ws, P, a) : launch_ws<false>(ctx, ws, P, a));
+      TRY(fast ? launch_ws_fast(ctx, ws, P, a) : launch_ws_exact(ctx, ws, P, a));
     } else if (which) {
       TiledArgs a{dx, wt, dy, c, h, w, k, OH, OW, 0, mode};
-      TRY(fast ? launch_tiled<true>(ctx, which, P, a, nb) : launch_tiled<false>(ctx, which, P, a, nb));
+      TRY(launch_tiled(ctx, fast, which, P, a, nb));
     } else {
       GenericArgs a{dx, dw, dy, nb, c, h, w, k, kh, kw, stride, OH, OW, pw, ph, ps, mode, PHo, PWo};
       const unsigned g = grid_for(size_t(nb) * y_img, 256, ctx->num_sms);
@@ -698,18 +454,11 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
     TRY(pack_count(nullptr, h, kh, stride, pool_h, pool_stride, &PHo));
     P = (pool_w == pool_h && pool_w == pool_stride) ? pool_w : -1;
   }
+  const int forced = (flags >> 8) & 0xff;
   const int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, c, OW, kh, kw, stride, P);
   const int which = (flags & SCONV_F_GENERIC) || ws ? 0 : pick_tiled(k, kh, kw, stride, P);
   if (ws) {
-    switch (ws) {
-      case 1: plan_ws<WsA<0>>(out, ws, n, k, OH, OW); break;
-      case 2: plan_ws<WsB<0>>(out, ws, n, k, OH, OW); break;
-      case 4: plan_ws<WsD<0>>(out, ws, n, k, OH, OW); break;
-      case 5: plan_ws<WsE<0>>(out, ws, n, k, OH, OW); break;
-      case 6: plan_ws<WsF<0>>(out, ws, n, k, OH, OW); break;
-      case 7: plan_ws<WsG<0>>(out, ws, n, k, OH, OW); break;
-      default: plan_ws<WsC<0>>(out, ws, n, k, OH, OW); break;
-    }
+    plan_ws(out, ws, n, k, OH, OW);
   } else if (which) {
     plan_for(out, which, n, k, OH, OW);
   } else {

@@ -117,10 +117,11 @@ def test_launch_plan(sc):
     assert p["kernel"] == 107 and p["smem_bytes"] <= 227 * 1024
     # K >= 128: v3 warp-specialised kernel, 7 consumer warps (4x4 tiles) + 1 producer
     p = sc.launch_plan(64, 512, 30, 30, 512, 3, 3, 1)
-    assert p["kernel"] == 101 and p["grid_y"] == 4 and p["block_threads"] == 256
-    assert p["grid_x"] == 64 * 7 * 7 // 7 and p["grid_z"] == 1
+    # linear grid, K-blocks fastest: (tiles / 7 CTAs) x 4 K-blocks
+    assert p["kernel"] == 101 and p["grid_y"] == 1 and p["block_threads"] == 256
+    assert p["grid_x"] == 64 * 7 * 7 // 7 * 4 and p["grid_z"] == 1
     p = sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1)  # 14x14 maps: 2x7 tiles, no waste
-    assert p["kernel"] == 102 and p["grid_x"] == 64 * 2 and p["grid_y"] == 4
+    assert p["kernel"] == 102 and p["grid_x"] == 64 * 2 * 4 and p["grid_y"] == 1
     assert sc.launch_plan(1, 20, 11, 11, 50, 5, 5, 1)["kernel"] == 0
 
 
