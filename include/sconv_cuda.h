@@ -135,6 +135,40 @@ int sconv_cu_pecr_conv_pool(sconv_cu_ctx* ctx, const float* x, int n, int c,
                             int pool_stride, int mode, float* y,
                             uint64_t* muls, uint64_t* adds, unsigned flags);
 
+/* ---- on-device multi-layer forward ------------------- */
+/* forward(net, input, method) of src/pipeline.cpp:212-301 for N images, with
+ * every activation resident in HBM: one ingest of the input and all filters,
+ * one egress of the output (plus any per-layer outputs requested).  Layer l:
+ *   PECR method, pooled layer with ReLU -> fused conv+ReLU+pool
+ *     (sconv_cu_pecr_conv_pool; the pre-pool output never reaches HBM);
+ *   otherwise -> ECR conv, ReLU (fused into the conv epilogue unless
+ *     conv_outputs[l] asks for the pre-activation map), then pool() if the
+ *     layer pools; pecr_fallback[l] = 1 for these layers under PECR
+ *     (ForwardResult::pecr_fallback_layers).
+ * Validation follows NetworkSpec::validate (pipeline.cpp:154-189); a layer
+ * that then fails (e.g. Eq. 3 not integral under PECR) is a ConfigError
+ * "layer l failed: ..." (pipeline.cpp:293-297).  The dense method is the CPU
+ * reference's and is refused (ConfigError).  With SCONV_F_DEVICE every
+ * pointer (x, filters, y, layer/conv outputs) is a device pointer.
+ * layer_outputs / conv_outputs: NULL or nlayers pointers, each NULL or a
+ * buffer for [N][k][..] of that layer (conv_outputs of fused layers are not
+ * written: the reference stores a 1x1x1 placeholder there). */
+#define SCONV_METHOD_ECR 1
+#define SCONV_METHOD_PECR 2
+typedef struct {
+  const float* filters; /* [k][c][kh][kw], c = the previous layer's k */
+  int k, kh, kw, stride;
+  int relu;             /* Activation::kRelu */
+  int pool_w, pool_h, pool_stride, pool_mode; /* pool_w == 0: LayerKind::kConv */
+} sconv_layer;
+int sconv_cu_forward_dims(const sconv_layer* layers, int nlayers, int c, int h,
+                          int w, int* out_c, int* out_h, int* out_w);
+int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h,
+                     int w, const sconv_layer* layers, int nlayers, int method,
+                     float* y, float* const* layer_outputs,
+                     float* const* conv_outputs, uint64_t* muls,
+                     uint64_t* adds, int32_t* pecr_fallback, unsigned flags);
+
 /* ---- formats: the reference's two-phase API (one map, one filter) ------- */
 /* ecr_convert (src/ecr.cpp:51-97) by warp-ballot compaction.  Writes the
  * fixed-slot EcrMap arrays of include/sconv/ecr.hpp:35-45, flattened

@@ -239,6 +239,46 @@ class COracle(_Lib):
         v = _f32(v).reshape(-1)
         return "%016x" % self.lib.orc_checksum(v, v.size)
 
+    def forward(self, x, layers, method):
+        """forward() of src/pipeline.cpp:212-301 for one image x [C,H,W],
+        composed from this oracle's restated primitives.  `layers`: dicts
+        {"filters": [K,C,kh,kw], "stride", "relu", "pool": (pw, ph, ps, mode)
+        or None}; method 0 dense / 1 ECR / 2 PECR.  Returns (output,
+        layer_outputs, conv_outputs, (muls, adds), pecr_fallback_layers);
+        conv_outputs[l] is None where the reference stores its 1x1x1
+        placeholder (fused layers, pipeline.cpp:258)."""
+        cur = _f32(x)
+        lo, co, fb = [], [], []
+        m = a = 0
+        for l, lay in enumerate(layers):
+            w = _f32(lay["filters"])
+            s = lay.get("stride", 1)
+            relu = lay.get("relu", True)
+            pool = lay.get("pool")
+            fuse = method == 2 and pool is not None and relu          # :238-240
+            if fuse:                                                   # :249-264
+                y, (dm, da) = self.pecr_conv(cur[None], w, s, pool[0], pool[1], pool[2], pool[3])
+                co.append(None)
+                cur = y[0]
+            else:
+                if method == 2:
+                    fb.append(l)                                       # :266-268
+                if method == 0:                                        # :241-248
+                    outs = [self.dense_conv(cur, w[k], s) for k in range(w.shape[0])]
+                    conv = np.stack([o[0] for o in outs])
+                    dm, da = sum(o[1][0] for o in outs), sum(o[1][1] for o in outs)
+                else:                                                  # :269-285
+                    y, (dm, da) = self.ecr_conv(cur[None], w, s)
+                    conv = y[0]
+                co.append(conv)
+                cur = self.relu(conv) if relu else conv
+                if pool is not None:
+                    cur = self.pool(cur, pool[0], pool[1], pool[2], pool[3])
+            m += dm
+            a += da
+            lo.append(cur)
+        return cur, lo, co, (m, a), fb
+
 
 class RefLib(_Lib):
     """The unmodified reference library through oracle/ref_bridge.cpp."""
@@ -267,6 +307,8 @@ class RefLib(_Lib):
         L.ref_checksum.argtypes = [_f32p, C.c_int64, C.c_char_p]
         L.ref_plan.argtypes = [C.c_int] * 10 + [C.POINTER(C.c_int), C.POINTER(C.c_int), _u64p]
         L.ref_hardware_concurrency.restype = C.c_int
+        L.ref_forward.argtypes = [_f32p] + [C.c_int] * 4 + [C.c_void_p] * 10 + [C.c_int, C.c_int,
+                                  _f32p, _f32p, _u64p, _u64p, C.c_void_p]
 
     def _chk(self, rc):
         if rc:
@@ -274,6 +316,50 @@ class RefLib(_Lib):
 
     def hardware_concurrency(self):
         return self.lib.ref_hardware_concurrency()
+
+    def forward(self, x, layers, method, workers=1):
+        """sconv::forward (pipeline.cpp:212-301) of the unmodified reference on
+        one image; same return shape as COracle.forward."""
+        x = _f32(x)
+        Cc, H, W = x.shape
+        nl = len(layers)
+        I = C.c_int * nl
+        ks, khs, kws, ss, rl = I(), I(), I(), I(), I()
+        pws, phs, pss, pms = I(), I(), I(), I()
+        fl = (C.c_void_p * nl)()
+        keep = []
+        sizes, csizes = [], []
+        h, w_ = H, W
+        for l, lay in enumerate(layers):
+            f = _f32(lay["filters"])
+            keep.append(f)
+            K, _, kh, kw = f.shape
+            s = lay.get("stride", 1)
+            ks[l], khs[l], kws[l], ss[l], rl[l] = K, kh, kw, s, int(lay.get("relu", True))
+            pool = lay.get("pool")
+            oh, ow = out_dims(h, w_, kh, kw, s)
+            csizes.append((K, oh, ow))
+            if pool is not None:
+                pws[l], phs[l], pss[l], pms[l] = pool
+                oh, ow = out_dims(oh, ow, pool[1], pool[0], pool[2])
+            fl[l] = f.ctypes.data
+            sizes.append((K, oh, ow))
+            h, w_ = oh, ow
+        lo_buf = np.zeros(sum(k * a * b for k, a, b in sizes), np.float32)
+        co_buf = np.zeros(sum(k * a * b for k, a, b in csizes), np.float32)
+        m, a = C.c_uint64(0), C.c_uint64(0)
+        fb = (C.c_int * nl)()
+        self._chk(self.lib.ref_forward(x.reshape(-1), Cc, H, W, nl, ks, khs, kws, ss, rl, pws, phs,
+                                       pss, pms, fl, method, workers, lo_buf, co_buf, C.byref(m),
+                                       C.byref(a), fb))
+        lo, co, p, q = [], [], 0, 0
+        for l, ((k, oh, ow), (ck, ch, cw)) in enumerate(zip(sizes, csizes)):
+            lo.append(lo_buf[p:p + k * oh * ow].reshape(k, oh, ow))
+            p += k * oh * ow
+            fused = method == 2 and layers[l].get("pool") is not None and layers[l].get("relu", True)
+            co.append(None if fused else co_buf[q:q + ck * ch * cw].reshape(ck, ch, cw))
+            q += ck * ch * cw
+        return lo[-1], lo, co, (m.value, a.value), [l for l in range(nl) if fb[l]]
 
     def rng(self, seed, n):
         out = np.empty(n, np.uint64)

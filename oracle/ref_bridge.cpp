@@ -17,6 +17,7 @@
 #include "sconv/errors.hpp"
 #include "sconv/exec.hpp"
 #include "sconv/pecr.hpp"
+#include "sconv/pipeline.hpp"
 #include "sconv/report.hpp"
 #include "sconv/tensor.hpp"
 
@@ -257,6 +258,58 @@ int ref_plan(int in_w, int in_h, int k_w, int k_h, int stride, int channels, int
     *blocks = g.blocks;
     *threads = g.threads_per_block;
     *smem = g.shared_bytes_per_block;
+  });
+}
+
+// forward (pipeline.cpp:212-301) over a network given as flat arrays; writes
+// every layer output (concatenated) and every conv output (concatenated, each
+// at its conv-output size; fused layers' 1x1x1 placeholders leave theirs 0).
+int ref_forward(const float* x, int C, int H, int W, int nl, const int* k, const int* kh,
+                const int* kw, const int* stride, const int* relu, const int* pw, const int* ph,
+                const int* ps, const int* pmode, const float* const* filters, int method,
+                int workers, float* layer_out, float* conv_out, uint64_t* muls, uint64_t* adds,
+                int* fallback) {
+  return guarded([&] {
+    NetworkSpec net;
+    net.in_channels = C;
+    net.in_height = H;
+    net.in_width = W;
+    int c = C;
+    for (int l = 0; l < nl; ++l) {
+      LayerSpec L;
+      for (int f = 0; f < k[l]; ++f)
+        L.filters.push_back(as_filter(filters[l] + static_cast<std::size_t>(f) * c * kh[l] * kw[l],
+                                      c, kh[l], kw[l]));
+      L.conv.stride = stride[l];
+      L.activation = relu[l] ? Activation::kRelu : Activation::kNone;
+      if (pw[l] > 0) {
+        L.kind = LayerKind::kConvPool;
+        L.pool = PoolConfig{pw[l], ph[l], ps[l], pmode[l] == 0 ? PoolMode::kMax : PoolMode::kMean};
+      }
+      net.layers.push_back(std::move(L));
+      c = k[l];
+    }
+    ExecConfig ex;
+    ex.workers = workers;
+    const Method m = method == 0 ? Method::kDense : method == 1 ? Method::kEcr : Method::kPecr;
+    const ForwardResult r = forward(net, as_map(x, C, H, W), m, ex);
+    std::size_t p = 0, q = 0;
+    int ih = H, iw = W;
+    for (int l = 0; l < nl; ++l) {
+      const auto& v = r.layer_outputs[l].values;
+      std::memcpy(layer_out + p, v.data(), v.size() * sizeof(float));
+      p += v.size();
+      const bool fused = m == Method::kPecr && pw[l] > 0 && relu[l];
+      const auto& cv = r.conv_outputs[l].values;
+      if (!fused) std::memcpy(conv_out + q, cv.data(), cv.size() * sizeof(float));
+      q += static_cast<std::size_t>(k[l]) * ((ih - kh[l]) / stride[l] + 1) *
+           ((iw - kw[l]) / stride[l] + 1);
+      ih = r.layer_outputs[l].height;
+      iw = r.layer_outputs[l].width;
+      fallback[l] = 0;
+    }
+    for (int l : r.pecr_fallback_layers) fallback[l] = 1;
+    add_ops(r.ops, muls, adds);
   });
 }
 

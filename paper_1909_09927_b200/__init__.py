@@ -10,7 +10,9 @@ from .api import (ConvConfig, EcrBlockRow, EcrDims, EcrGridShape, EcrMap, ExecCo
                   PoolMode, checksum_hex, conv_output_dims, ecr_conv_batched, ecr_convert,
                   ecr_grid_shape, ecr_spmv_conv, ecr_window, generate, generate_batch,
                   launch_plan, multichannel_conv, pecr_conv_pool, pecr_conv_pool_batched,
-                  pecr_convert, pecr_pack_count, pecr_window, shard)
+                  pecr_convert, pecr_pack_count, pecr_window, shard, Activation, LayerKind,
+                  Method, LayerSpec, NetworkSpec, ForwardResult, TrafficReport, forward,
+                  forward_batched)
 from ._native import LIB_PATH, SYMBOLS, Context, context
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -24,6 +24,7 @@ SYMBOLS = (
     "sconv_cu_pecr_conv_pool", "sconv_cu_ecr_convert", "sconv_cu_ecr_spmv", "sconv_cu_pecr_count",
     "sconv_cu_pecr_fill", "sconv_cu_pecr_pool", "sconv_shard", "sconv_cu_ecr_conv_multi",
     "sconv_cu_pecr_conv_pool_multi", "sconv_generate", "sconv_generate_batch", "sconv_checksum",
+    "sconv_cu_forward", "sconv_cu_forward_dims",
 )
 
 F_EXACT = 0
@@ -42,6 +43,16 @@ def F_KERNEL(kid) -> int:
 _vp = C.c_void_p
 _i = C.c_int
 _u64p = C.POINTER(C.c_uint64)
+
+
+METHOD_ECR = 1
+METHOD_PECR = 2
+
+
+class LayerDesc(C.Structure):
+    """sconv_layer (include/sconv_cuda.h)."""
+    _fields_ = [("filters", _vp), ("k", _i), ("kh", _i), ("kw", _i), ("stride", _i), ("relu", _i),
+                ("pool_w", _i), ("pool_h", _i), ("pool_stride", _i), ("pool_mode", _i)]
 
 
 class LaunchPlan(C.Structure):
@@ -95,6 +106,9 @@ def lib() -> C.CDLL:
         _i] * 4 + [_vp, _u64p, _u64p, C.c_uint]
     L.sconv_cu_pecr_conv_pool_multi.argtypes = [C.POINTER(_vp), _i, _vp] + [_i] * 4 + [_vp] + [
         _i] * 8 + [_vp, _u64p, _u64p, C.c_uint]
+    L.sconv_cu_forward_dims.argtypes = [_vp, _i, _i, _i, _i] + [C.POINTER(_i)] * 3
+    L.sconv_cu_forward.argtypes = [_vp, _vp] + [_i] * 4 + [_vp, _i, _i, _vp, _vp, _vp, _u64p,
+                                                           _u64p, _vp, C.c_uint]
     L.sconv_generate.argtypes = [_i, _i, _i, C.c_double, C.c_uint64, _vp]
     L.sconv_generate_batch.argtypes = [_i, _i, _i, _i, C.c_double, _vp, _vp, _i]
     L.sconv_checksum.argtypes = [_vp, C.c_int64]

@@ -586,6 +586,238 @@ def multichannel_conv(map: FeatureMap, filters: Sequence[Filter], cfg: ConvConfi
 
 
 # ---------------------------------------------------------------------------
+# on-device multi-layer forward (include/sconv/pipeline.hpp, src/pipeline.cpp)
+# ---------------------------------------------------------------------------
+
+
+class Activation(enum.IntEnum):
+    kNone = 0
+    kRelu = 1
+
+
+class LayerKind(enum.IntEnum):
+    kConv = 0
+    kConvPool = 1
+
+
+class Method(enum.IntEnum):
+    kDense = 0
+    kEcr = 1
+    kPecr = 2
+
+
+@dataclass
+class TrafficReport:
+    """Modeled byte traffic (include/sconv/metrics.hpp:26-48)."""
+    host_to_device_bytes: int = 0
+    device_to_host_bytes: int = 0
+    global_loads_bytes: int = 0
+    global_stores_bytes: int = 0
+
+
+@dataclass
+class LayerSpec:
+    """pipeline.hpp:18-24: filters share dims; kConvPool requires `pool`."""
+    kind: LayerKind = LayerKind.kConv
+    filters: Sequence[Filter] = ()
+    conv: ConvConfig = field(default_factory=ConvConfig)
+    pool: Optional[PoolConfig] = None
+    activation: Activation = Activation.kRelu
+
+
+@dataclass
+class NetworkSpec:
+    in_channels: int = 0
+    in_height: int = 0
+    in_width: int = 0
+    layers: List[LayerSpec] = field(default_factory=list)
+
+    def validate(self) -> None:
+        """NetworkSpec::validate (pipeline.cpp:154-189)."""
+        if self.in_channels < 1 or self.in_height < 1 or self.in_width < 1:
+            raise ConfigError("network input dims must be positive")
+        if not self.layers:
+            raise ConfigError("network has no layers")
+        c, h, w = self.in_channels, self.in_height, self.in_width
+        for l, layer in enumerate(self.layers):
+            where = f"layer {l}: "
+            if not layer.filters:
+                raise ConfigError(where + "no filters")
+            f0 = layer.filters[0]
+            for f in layer.filters:
+                if (f.channels, f.height, f.width) != (f0.channels, f0.height, f0.width):
+                    raise ConfigError(where + "filters have mismatched dims")
+            if f0.channels != c:
+                raise ConfigError(where + f"filter channels {f0.channels} != input channels {c}")
+            if layer.conv.stride < 1:
+                raise ConfigError(where + "conv stride must be >= 1")
+            if layer.kind == LayerKind.kConvPool and layer.pool is None:
+                raise ConfigError(where + "conv_pool layer without pool config")
+            if layer.kind == LayerKind.kConv and layer.pool is not None:
+                raise ConfigError(where + "conv layer with pool config")
+            od = conv_output_dims(w, h, f0.width, f0.height, layer.conv.stride)
+            h, w = od.height, od.width
+            if layer.pool is not None:
+                pd = conv_output_dims(w, h, layer.pool.width, layer.pool.height, layer.pool.stride)
+                h, w = pd.height, pd.width
+            c = len(layer.filters)
+
+
+@dataclass
+class ForwardResult:
+    """pipeline.hpp:37-50."""
+    output: FeatureMap
+    ops: OpCount = field(default_factory=OpCount)
+    traffic: TrafficReport = field(default_factory=TrafficReport)
+    conv_outputs: List[FeatureMap] = field(default_factory=list)
+    layer_outputs: List[FeatureMap] = field(default_factory=list)
+    pecr_fallback_layers: List[int] = field(default_factory=list)
+
+
+def _layer_descs(layers_w, layer_cfg):
+    """(filters [K,C,kh,kw] pointer/array, cfg dict) -> LayerDesc array."""
+    arr = (nat.LayerDesc * len(layer_cfg))()
+    for l, (wp, cfg) in enumerate(zip(layers_w, layer_cfg)):
+        d = arr[l]
+        d.filters = wp
+        d.k, d.kh, d.kw = cfg["k"], cfg["kh"], cfg["kw"]
+        d.stride = cfg["stride"]
+        d.relu = int(cfg["relu"])
+        pool = cfg.get("pool")
+        if pool is not None:
+            d.pool_w, d.pool_h, d.pool_stride, d.pool_mode = (pool.width, pool.height, pool.stride,
+                                                              int(pool.mode))
+    return arr
+
+
+def forward_batched(x, layers: Sequence[dict], method: Method = Method.kPecr, *,
+                    fast: bool = False, counters: Optional[OpCount] = None,
+                    device: Optional[int] = None, generic: bool = False,
+                    layer_outputs: bool = False, conv_outputs: bool = False, kernel=0):
+    """forward() of src/pipeline.cpp:212-301 for a batch x [N,C,H,W] with every
+    activation resident on the GPU (sconv_cu_forward).  `layers` is a list of
+    dicts {"filters": [K,C,kh,kw], "stride": s, "relu": bool, "pool":
+    PoolConfig or None}.  numpy in -> numpy out; torch CUDA in -> torch out.
+    Returns (output, layer_outputs list or None, conv_outputs list or None,
+    pecr_fallback_layers)."""
+    L = nat.lib()
+    if int(method) == Method.kDense:
+        raise ConfigError("forward on the GPU runs the compressed methods (ECR, PECR); the dense "
+                          "method is the CPU reference's")
+    flags = (nat.F_FAST if fast else 0) | (nat.F_GENERIC if generic else 0)
+    if kernel:
+        flags |= nat.F_KERNEL(kernel)
+    torch_in = _is_torch_cuda(x)
+    if torch_in:
+        import torch
+        x = x.contiguous()
+        ws = [lay["filters"].contiguous() for lay in layers]
+        dev = x.device.index if device is None else device
+        N, Cc, H, W = x.shape
+    else:
+        x = np.ascontiguousarray(x, np.float32)
+        ws = [np.ascontiguousarray(lay["filters"], np.float32) for lay in layers]
+        dev = 0 if device is None else device
+        N, Cc, H, W = x.shape
+    cfg = []
+    for lay, w in zip(layers, ws):
+        K, Cf, kh, kw = w.shape
+        cfg.append({"k": K, "kh": kh, "kw": kw, "stride": lay.get("stride", 1),
+                    "relu": lay.get("relu", True), "pool": lay.get("pool")})
+    descs = _layer_descs([0] * len(cfg), cfg)
+    oc, oh, ow = C.c_int(), C.c_int(), C.c_int()
+    nat.check(L.sconv_cu_forward_dims(descs, len(cfg), Cc, H, W, C.byref(oc), C.byref(oh),
+                                      C.byref(ow)))
+    # per-layer dims (for the optional outputs)
+    dims, c, h, w_ = [], Cc, H, W
+    for cf in cfg:
+        od = conv_output_dims(w_, h, cf["kw"], cf["kh"], cf["stride"])
+        pd = od
+        if cf["pool"] is not None:
+            pd = conv_output_dims(od.width, od.height, cf["pool"].width, cf["pool"].height,
+                                  cf["pool"].stride)
+        dims.append((cf["k"], od.height, od.width, pd.height, pd.width))
+        c, h, w_ = cf["k"], pd.height, pd.width
+    if torch_in:
+        mk = lambda shape: torch.empty(shape, dtype=torch.float32, device=x.device)
+        ptr = lambda t: t.data_ptr()
+        ctx = nat.context(dev)
+        ctx.set_stream(torch.cuda.current_stream(x.device).cuda_stream)
+        flags |= nat.F_DEVICE
+    else:
+        mk = lambda shape: np.empty(shape, np.float32)
+        ptr = _ptr
+        ctx = nat.context(dev)
+        ctx.use_own_stream()
+    descs = _layer_descs([ptr(w) for w in ws], cfg)
+    out = mk((N, oc.value, oh.value, ow.value))
+    lo = [mk((N, k, ph, pw)) for k, _, _, ph, pw in dims] if layer_outputs else None
+    fused = [int(method) == Method.kPecr and cf["pool"] is not None and cf["relu"] for cf in cfg]
+    co = ([None if fz else mk((N, k, h2, w2)) for fz, (k, h2, w2, _, _) in zip(fused, dims)]
+          if conv_outputs else None)
+    P = C.c_void_p * len(cfg)
+    lo_arr = P(*[ptr(t) for t in lo]) if lo else None
+    co_arr = P(*[ptr(t) if t is not None else None for t in co]) if co else None
+    fb = (C.c_int32 * len(cfg))()
+    m, a = C.c_uint64(0), C.c_uint64(0)
+    mp = C.byref(m) if counters is not None else None
+    ap = C.byref(a) if counters is not None else None
+    st = L.sconv_cu_forward(ctx.handle, ptr(x), N, Cc, H, W, descs, len(cfg), int(method),
+                            ptr(out), lo_arr, co_arr, mp, ap, fb, flags)
+    nat.check(st, ctx.handle)
+    if counters is not None:
+        counters.merge(OpCount(m.value, a.value))
+    return out, lo, co, [l for l in range(len(cfg)) if fb[l]]
+
+
+def forward(net: NetworkSpec, input: FeatureMap, method: Method,
+            exec: ExecConfig = ExecConfig()) -> ForwardResult:
+    """GPU forward (pipeline.cpp:212-301): ForwardResult with output, ops,
+    per-layer conv/layer outputs, pecr_fallback_layers and the modeled
+    traffic of the compressed methods (pipeline.cpp:222-289)."""
+    net.validate()
+    if (input.channels, input.height, input.width) != (net.in_channels, net.in_height,
+                                                        net.in_width):
+        raise ShapeError("input dims do not match network spec")
+    if exec.workers < 1:
+        raise ConfigError("workers must be >= 1")
+    layers = [{"filters": np.stack([f.array() for f in lay.filters]), "stride": lay.conv.stride,
+               "relu": lay.activation == Activation.kRelu, "pool": lay.pool}
+              for lay in net.layers]
+    ops = OpCount()
+    y, lo, co, fb = forward_batched(input.array()[None], layers, method, fast=exec.fast,
+                                    counters=ops, device=exec.device, layer_outputs=True,
+                                    conv_outputs=True)
+    res = ForwardResult(output=FeatureMap(y.shape[1], y.shape[2], y.shape[3], y.reshape(-1)),
+                        ops=ops, pecr_fallback_layers=fb)
+    mb = lambda c, h, w: 4 * c * h * w
+    t = res.traffic
+    t.host_to_device_bytes = mb(input.channels, input.height, input.width) + sum(
+        4 * sum(f.size for f in lay.filters) for lay in net.layers)
+    cur = (input.channels, input.height, input.width)
+    for l, lay in enumerate(net.layers):
+        fbytes = 4 * sum(f.size for f in lay.filters)
+        conv = co[l]
+        out = lo[l]
+        res.layer_outputs.append(FeatureMap(out.shape[1], out.shape[2], out.shape[3],
+                                            out.reshape(-1)))
+        t.global_loads_bytes += mb(*cur) + fbytes
+        if conv is None:  # fused: the reference stores a 1x1x1 placeholder
+            res.conv_outputs.append(FeatureMap(1, 1, 1))
+        else:
+            res.conv_outputs.append(FeatureMap(conv.shape[1], conv.shape[2], conv.shape[3],
+                                               conv.reshape(-1)))
+            t.global_stores_bytes += mb(conv.shape[1], conv.shape[2], conv.shape[3])
+            if lay.pool is not None:
+                t.global_loads_bytes += mb(conv.shape[1], conv.shape[2], conv.shape[3])
+        if conv is None or lay.pool is not None:
+            t.global_stores_bytes += mb(out.shape[1], out.shape[2], out.shape[3])
+        cur = (out.shape[1], out.shape[2], out.shape[3])
+    t.device_to_host_bytes = mb(*cur)
+    return res
+
+
+# ---------------------------------------------------------------------------
 # datasets / reports / planning
 # ---------------------------------------------------------------------------
 

@@ -24,6 +24,8 @@ struct sconv_cu_ctx {
   int smem_optin = 0;
   cudaStream_t aux = nullptr;       // second stream of the chunked host-pointer pipeline
   cudaEvent_t ev_w = nullptr, ev_done = nullptr;
+  char* fwd = nullptr;              // sconv_cu_forward: resident activations + filters
+  size_t fwd_cap = 0;
 };
 
 namespace sconv_cu {

@@ -58,6 +58,21 @@ struct PoolFold {
   }
 };
 
+// Activation::kRelu applied in an ECR epilogue (relu(), src/tensor.cpp:89-95:
+// v > 0 ? v : +0, so -0 and NaN become +0).  For P == 0 launches the `mode`
+// argument (the pool mode of PECR launches) carries this flag.
+__device__ __forceinline__ float relu_f(float v) { return v > 0.0f ? v : 0.0f; }
+
+template <int A, int B, int R>
+__device__ __forceinline__ void relu_tile(float (&acc)[A][B][R]) {
+#pragma unroll
+  for (int i = 0; i < A; ++i)
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[i][j][r] = relu_f(acc[i][j][r]);
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 __device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool valid) {

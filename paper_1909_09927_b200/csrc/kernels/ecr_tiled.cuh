@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(Cfg::NT, MINB) ecr_tiled_kernel(const TiledArg
   // ---- epilogue ----------------------------------------------------------
   const int kw0 = k0 + wk * 32 * R;
   if constexpr (P == 0) {
+    if (a.mode) relu_tile(acc);  // fused Activation::kRelu (forward)
     const int gx0 = ox0 + wsx * TW;
     const bool vec = (a.OW % 4 == 0) && (TW % 4 == 0);
 #pragma unroll

@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
   // ---- epilogue ------------------------------------------------------------
   const int oy0 = ty * TH, ox0 = tx * TW;
   if constexpr (P == 0) {
+    if (a.mode) relu_tile(acc);  // fused Activation::kRelu (forward)
     const bool vec = (TW % 4 == 0) && (a.OW % 4 == 0);
 #pragma unroll
     for (int r = 0; r < R; ++r) {

@@ -13,7 +13,7 @@ struct GenericArgs {
   const float* w;  // [K][C][kh][kw]
   float* y;
   int N, C, H, W, K, kh, kw, S, OH, OW;
-  int pw, ph, ps, mode;  // PECR only
+  int pw, ph, ps, mode;  // PECR pool geometry; mode = pool mode (PECR) / fused ReLU (ECR)
   int PH, PW;            // PECR pack grid
 };
 
@@ -45,7 +45,8 @@ __global__ void ecr_generic_kernel(const GenericArgs a) {
     const int n = static_cast<int>(idx / (static_cast<size_t>(a.OW) * a.OH * a.K));
     const float* xn = a.x + static_cast<size_t>(n) * a.C * a.H * a.W;
     const float* wk = a.w + static_cast<size_t>(k) * a.C * a.kh * a.kw;
-    a.y[idx] = window_dot<FAST>(xn, wk, a.C, a.H, a.W, a.kh, a.kw, oy * a.S, ox * a.S);
+    const float v = window_dot<FAST>(xn, wk, a.C, a.H, a.W, a.kh, a.kw, oy * a.S, ox * a.S);
+    a.y[idx] = a.mode ? relu_f(v) : v;  // mode = fused ReLU for ECR launches
   }
 }
 
@@ -83,6 +84,43 @@ __global__ void transpose_filters_kernel(const float* __restrict__ w, float* __r
     const int k = static_cast<int>(idx % Kp);
     const size_t cij = idx / Kp;  // c*KK + ij
     wt[idx] = k < K ? __ldg(w + static_cast<size_t>(k) * C * KK + cij) : 0.0f;
+  }
+}
+
+// ReLU in place (Activation::kRelu after an unfused conv).
+__global__ void relu_kernel(float* __restrict__ v, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    v[i] = relu_f(v[i]);
+}
+
+// pool() of src/tensor.cpp:97-129 over [N*C] planes of H x W: max starts from
+// the window's first element and keeps `v > best`; mean sums in raster order
+// and divides by the window count.  Output dims use conv_output_dims (floor).
+__global__ void pool_kernel(const float* __restrict__ x, float* __restrict__ y, size_t planes,
+                            int H, int W, int pw, int ph, int ps, int mode, int OH, int OW) {
+  const size_t total = planes * OH * OW;
+  const float count = static_cast<float>(pw * ph);
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int ox = static_cast<int>(idx % OW);
+    const int oy = static_cast<int>((idx / OW) % OH);
+    const size_t pl = idx / (static_cast<size_t>(OW) * OH);
+    const float* xp = x + pl * H * W + static_cast<size_t>(oy * ps) * W + ox * ps;
+    if (mode == 0) {
+      float best = xp[0];
+      for (int i = 0; i < ph; ++i)
+        for (int j = 0; j < pw; ++j) {
+          const float v = xp[i * W + j];
+          if (v > best) best = v;
+        }
+      y[idx] = best;
+    } else {
+      float sum = 0.0f;
+      for (int i = 0; i < ph; ++i)
+        for (int j = 0; j < pw; ++j) sum = __fadd_rn(sum, xp[i * W + j]);
+      y[idx] = __fdiv_rn(sum, count);
+    }
   }
 }
 

@@ -388,6 +388,7 @@ int sconv_cu_ctx_destroy(sconv_cu_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->aux) cudaStreamSynchronize(ctx->aux);
     if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->fwd) cudaFree(ctx->fwd);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->ev_w) cudaEventDestroy(ctx->ev_w);
@@ -469,6 +470,181 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
     out->block_threads = 256;
     out->tile_h = out->tile_w = out->tile_k = 1;
   }
+  return SCONV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// On-device multi-layer forward (forward(), src/pipeline.cpp:212-301)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct FwdLayerDims {
+  int c, h, w;     // input
+  int oh, ow;      // conv output
+  int ph, pw;      // after pool (== oh, ow without pool)
+};
+
+// NetworkSpec::validate (src/pipeline.cpp:154-189) with the reference's error
+// types, plus every layer's dims.
+int forward_plan(sconv_cu_ctx* ctx, const sconv_layer* layers, int nl, int c, int h, int w,
+                 std::vector<FwdLayerDims>* dims) {
+  if (c < 1 || h < 1 || w < 1) return fail(ctx, SCONV_ERR_CONFIG, "network input dims must be positive");
+  if (nl < 1 || !layers) return fail(ctx, SCONV_ERR_CONFIG, "network has no layers");
+  dims->clear();
+  for (int l = 0; l < nl; ++l) {
+    const sconv_layer& L = layers[l];
+    if (L.k < 1) return fail(ctx, SCONV_ERR_CONFIG, "layer %d: no filters", l);
+    if (L.stride < 1) return fail(ctx, SCONV_ERR_CONFIG, "layer %d: conv stride must be >= 1", l);
+    FwdLayerDims d{c, h, w, 0, 0, 0, 0};
+    TRY(conv_dims(ctx, w, h, L.kw, L.kh, L.stride, &d.ow, &d.oh));
+    d.pw = d.ow;
+    d.ph = d.oh;
+    if (L.pool_w != 0 || L.pool_h != 0) {
+      if (L.pool_w < 1 || L.pool_h < 1) return fail(ctx, SCONV_ERR_SHAPE, "pool window must be positive");
+      if (L.pool_stride < 1) return fail(ctx, SCONV_ERR_CONFIG, "pool stride must be >= 1");
+      if (L.pool_mode != SCONV_POOL_MAX && L.pool_mode != SCONV_POOL_MEAN)
+        return fail(ctx, SCONV_ERR_CONFIG, "layer %d: unknown pool mode %d", l, L.pool_mode);
+      TRY(conv_dims(ctx, d.ow, d.oh, L.pool_w, L.pool_h, L.pool_stride, &d.pw, &d.ph));
+    }
+    dims->push_back(d);
+    c = L.k;
+    h = d.ph;
+    w = d.pw;
+  }
+  return SCONV_OK;
+}
+
+}  // namespace
+
+int sconv_cu_forward_dims(const sconv_layer* layers, int nlayers, int c, int h, int w, int* out_c,
+                          int* out_h, int* out_w) {
+  std::vector<FwdLayerDims> dims;
+  TRY(forward_plan(nullptr, layers, nlayers, c, h, w, &dims));
+  if (out_c) *out_c = layers[nlayers - 1].k;
+  if (out_h) *out_h = dims.back().ph;
+  if (out_w) *out_w = dims.back().pw;
+  return SCONV_OK;
+}
+
+int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w,
+                     const sconv_layer* layers, int nlayers, int method, float* y,
+                     float* const* layer_outputs, float* const* conv_outputs, uint64_t* muls,
+                     uint64_t* adds, int32_t* pecr_fallback, unsigned flags) {
+  if (!ctx) return fail(nullptr, SCONV_ERR_ARG, "null context");
+  if (method != SCONV_METHOD_ECR && method != SCONV_METHOD_PECR)
+    return fail(ctx, SCONV_ERR_CONFIG,
+                "forward on the GPU runs the compressed methods (ECR, PECR); the dense method is "
+                "the CPU reference's");
+  if (n < 0) return fail(ctx, SCONV_ERR_SHAPE, "negative batch");
+  if (flags & SCONV_F_ASYNC) return fail(ctx, SCONV_ERR_ARG, "forward is synchronous");
+  std::vector<FwdLayerDims> dims;
+  TRY(forward_plan(ctx, layers, nlayers, c, h, w, &dims));
+  if (n == 0) return SCONV_OK;
+  if (!x || !y) return fail(ctx, SCONV_ERR_ARG, "null tensor pointer");
+  for (int l = 0; l < nlayers; ++l)
+    if (!layers[l].filters) return fail(ctx, SCONV_ERR_ARG, "layer %d: null filters", l);
+  const bool dev = flags & SCONV_F_DEVICE;
+  const bool counters = muls || adds;
+
+  // device residency: input, every layer's filters (host pointers only),
+  // two activation buffers and one pre-pool conv buffer
+  size_t act = size_t(c) * h * w, conv = 0, wtot = 0;
+  for (int l = 0; l < nlayers; ++l) {
+    const FwdLayerDims& d = dims[l];
+    act = std::max(act, size_t(layers[l].k) * d.ph * d.pw);
+    conv = std::max(conv, size_t(layers[l].k) * d.oh * d.ow);
+    wtot += size_t(layers[l].k) * d.c * layers[l].kh * layers[l].kw;
+  }
+  auto up = [](size_t b) { return (b + 255) & ~size_t{255}; };
+  const size_t b_act = up(size_t(n) * act * 4), b_conv = up(size_t(n) * conv * 4);
+  const size_t b_w = dev ? 0 : up(wtot * 4);
+  const size_t need = 2 * b_act + b_conv + b_w;
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  if (need > ctx->fwd_cap) {
+    CK(cudaStreamSynchronize(st));
+    if (ctx->fwd) CK(cudaFree(ctx->fwd));
+    ctx->fwd = nullptr;
+    ctx->fwd_cap = 0;
+    CK(cudaMalloc(&ctx->fwd, need));
+    ctx->fwd_cap = need;
+  }
+  float* buf[2] = {reinterpret_cast<float*>(ctx->fwd), reinterpret_cast<float*>(ctx->fwd + b_act)};
+  float* cbuf = reinterpret_cast<float*>(ctx->fwd + 2 * b_act);
+  float* wdev = reinterpret_cast<float*>(ctx->fwd + 2 * b_act + b_conv);
+  std::vector<const float*> filt(nlayers);
+  {  // one-time ingest (forward's h2d accounting, pipeline.cpp:222-227)
+    size_t off = 0;
+    for (int l = 0; l < nlayers; ++l) {
+      const size_t cnt = size_t(layers[l].k) * dims[l].c * layers[l].kh * layers[l].kw;
+      if (dev) {
+        filt[l] = layers[l].filters;
+      } else {
+        CK(cudaMemcpyAsync(wdev + off, layers[l].filters, cnt * 4, cudaMemcpyHostToDevice, st));
+        filt[l] = wdev + off;
+      }
+      off += cnt;
+    }
+  }
+  const float* cur = x;
+  if (!dev) {
+    CK(cudaMemcpyAsync(buf[0], x, size_t(n) * c * h * w * 4, cudaMemcpyHostToDevice, st));
+    cur = buf[0];
+  }
+  const unsigned kflags = (flags & (SCONV_F_FAST | SCONV_F_GENERIC | (0xffu << 8))) | SCONV_F_DEVICE |
+                          (counters ? 0u : SCONV_F_ASYNC);
+  const cudaMemcpyKind out_kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  uint64_t m_acc = 0, a_acc = 0;
+  for (int l = 0; l < nlayers; ++l) {
+    const sconv_layer& L = layers[l];
+    const FwdLayerDims& d = dims[l];
+    const bool pooled = L.pool_w != 0;
+    const bool fuse = method == SCONV_METHOD_PECR && pooled && L.relu;
+    if (pecr_fallback) pecr_fallback[l] = method == SCONV_METHOD_PECR && !fuse;
+    float* next = buf[(cur == buf[0]) ? 1 : 0];
+    uint64_t* pm = counters ? &m_acc : nullptr;
+    uint64_t* pa = counters ? &a_acc : nullptr;
+    int rc;
+    const size_t conv_elems = size_t(n) * L.k * d.oh * d.ow;
+    if (fuse) {
+      rc = fused_conv(ctx, cur, n, d.c, d.h, d.w, filt[l], L.k, L.kh, L.kw, L.stride, L.pool_w,
+                      L.pool_h, L.pool_stride, L.pool_mode, next, pm, pa, kflags);
+    } else {
+      const bool want_conv = conv_outputs && conv_outputs[l];
+      // ReLU fused into the conv epilogue unless the pre-activation output is wanted
+      const int relu_in_epi = L.relu && !want_conv;
+      float* dst = pooled ? cbuf : next;
+      rc = fused_conv(ctx, cur, n, d.c, d.h, d.w, filt[l], L.k, L.kh, L.kw, L.stride, 0, 0, 1,
+                      relu_in_epi, dst, pm, pa, kflags);
+      if (rc == SCONV_OK && want_conv)
+        CK(cudaMemcpyAsync(conv_outputs[l], dst, conv_elems * 4, out_kind, st));
+      if (rc == SCONV_OK && L.relu && !relu_in_epi) {
+        relu_kernel<<<grid_for(conv_elems, 256, ctx->num_sms), 256, 0, st>>>(dst, conv_elems);
+        TRY(finish_launch(ctx, "relu_kernel"));
+      }
+      if (rc == SCONV_OK && pooled) {
+        const size_t planes = size_t(n) * L.k;
+        pool_kernel<<<grid_for(planes * d.ph * d.pw, 256, ctx->num_sms), 256, 0, st>>>(
+            cbuf, next, planes, d.oh, d.ow, L.pool_w, L.pool_h, L.pool_stride, L.pool_mode, d.ph,
+            d.pw);
+        TRY(finish_launch(ctx, "pool_kernel"));
+      }
+    }
+    if (rc != SCONV_OK) {
+      if (rc == SCONV_ERR_CUDA || rc == SCONV_ERR_ARG || rc == SCONV_ERR_DISPATCH) return rc;
+      // per-layer failures surface as ConfigError (pipeline.cpp:293-297)
+      const std::string why = ctx->err;
+      return fail(ctx, SCONV_ERR_CONFIG, "layer %d failed: %s", l, why.c_str());
+    }
+    const size_t out_elems = size_t(n) * L.k * d.ph * d.pw;
+    if (layer_outputs && layer_outputs[l])
+      CK(cudaMemcpyAsync(layer_outputs[l], next, out_elems * 4, out_kind, st));
+    if (l == nlayers - 1) CK(cudaMemcpyAsync(y, next, out_elems * 4, out_kind, st));
+    cur = next;
+  }
+  CK(cudaStreamSynchronize(st));
+  if (muls) *muls += m_acc;
+  if (adds) *adds += a_acc;
   return SCONV_OK;
 }
 
