@@ -793,10 +793,10 @@ def forward(net: NetworkSpec, input: FeatureMap, method: Method,
     mb = lambda c, h, w: 4 * c * h * w
     t = res.traffic
     t.host_to_device_bytes = mb(input.channels, input.height, input.width) + sum(
-        4 * sum(f.size for f in lay.filters) for lay in net.layers)
+        4 * sum(f.size() for f in lay.filters) for lay in net.layers)
     cur = (input.channels, input.height, input.width)
     for l, lay in enumerate(net.layers):
-        fbytes = 4 * sum(f.size for f in lay.filters)
+        fbytes = 4 * sum(f.size() for f in lay.filters)
         conv = co[l]
         out = lo[l]
         res.layer_outputs.append(FeatureMap(out.shape[1], out.shape[2], out.shape[3],
