@@ -215,6 +215,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also sweep sparsity (side file)")
+    ap.add_argument("--no-forward", action="store_true", help="skip the multi-layer forward leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -412,6 +413,8 @@ def main():
     if args.sweep and rank == 0:
         sweep_side_file(sc, torch, dev, fast)
 
+    fwd = None if args.no_forward else forward_side(sc, torch, dev, fast, rank)
+
     value = ms_per_step * 1e3 / nl / world
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -447,6 +450,7 @@ def main():
         "cudnn": cudnn or None,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "forward": fwd,
         "setup_s": t_gen,
     }
     if rank == 0:
@@ -454,6 +458,62 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+# VGG-19 on valid convolutions (the reference's forward() has no padding): a
+# 460x460 input gives VGG-19's block structure (2-2-4-4-4 convs, 2x2/2 max
+# pools after each block) and ends at 512 x 7 x 7.
+FWD_IN = 460
+FWD_BATCH = 16
+
+
+def vgg19_valid_layers():
+    chans = [(3, 64), (64, 64), (64, 128), (128, 128), (128, 256), (256, 256), (256, 256),
+             (256, 256), (256, 512), (512, 512), (512, 512), (512, 512), (512, 512), (512, 512),
+             (512, 512), (512, 512)]
+    pooled = {1, 3, 7, 11, 15}
+    return [(c, k, l in pooled) for l, (c, k) in enumerate(chans)]
+
+
+def forward_side(sc, torch, dev, fast, rank):
+    """forward(net, x, Method::kPecr) of pipeline.cpp:212-301 on the GPU
+    (sconv_cu_forward): VGG-19 (valid convs) with ReLU, the 5 pooled layers
+    fused (PECR), activations resident in HBM between layers.  Timed with CUDA
+    events on the context stream, device-resident input and filters."""
+    spec = vgg19_valid_layers()
+    layers = []
+    for l, (c, k, pooled) in enumerate(spec):
+        hw = torch.empty((k, c, 3, 3), dtype=torch.float32)
+        sc.generate_batch([2_000_000 * (l + 1) + j for j in range(k)], 3, 3, c, 0.0,
+                          out=hw.numpy())
+        hw -= 0.5
+        # scale so activations stay O(1) through 16 layers (He-style)
+        hw *= float((2.0 / (9 * c)) ** 0.5 / 0.29)
+        layers.append({"filters": hw.to(dev), "stride": 1, "relu": True,
+                       "pool": sc.PoolConfig(2, 2, 2) if pooled else None})
+    hx = torch.empty((FWD_BATCH, 3, FWD_IN, FWD_IN), dtype=torch.float32)
+    sc.generate_batch([3_000_000 + rank * FWD_BATCH + n for n in range(FWD_BATCH)], FWD_IN,
+                      FWD_IN, 3, 0.7, out=hx.numpy())
+    x = hx.to(dev)
+    run = lambda: sc.forward_batched(x, layers, sc.Method.kPecr, fast=fast)
+    y, _, _, fb = run()
+    run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    e0.record()
+    for _ in range(reps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nz = float((y != 0).float().mean().item())
+    return {"network": "VGG-19 valid convs (16 conv + ReLU, 5 fused 2x2/2 max pools), input "
+                       f"3x{FWD_IN}x{FWD_IN}, batch {FWD_BATCH} per GPU, input sparsity 0.7",
+            "ms_per_batch": ms, "images_per_s": FWD_BATCH / (ms * 1e-3),
+            "output_shape": list(y.shape), "pecr_fallback_layers": fb,
+            "output_nonzero_frac": nz,
+            "path": "sconv_cu_forward (one call, device pointers)"}
 
 
 def sweep_side_file(sc, torch, dev, fast):

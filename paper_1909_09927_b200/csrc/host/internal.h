@@ -22,8 +22,10 @@ struct sconv_cu_ctx {
   size_t ws_cap = 0;
   int num_sms = 148;
   int smem_optin = 0;
-  cudaStream_t aux = nullptr;       // second stream of the chunked host-pointer pipeline
-  cudaEvent_t ev_w = nullptr, ev_done = nullptr;
+  // host-pointer pipeline: copy streams and per-buffer events (fused_conv)
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_in[3] = {}, ev_comp[3] = {}, ev_out[3] = {};
+  cudaEvent_t ev_done = nullptr;
   char* fwd = nullptr;              // sconv_cu_forward: resident activations + filters
   size_t fwd_cap = 0;
 };

@@ -174,17 +174,20 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   const bool counters = muls || adds;
 
   DeviceGuard guard(ctx->device);
-  // Host pointers: the batch is cut into image chunks that alternate between
-  // two streams with their own device buffers, so the H2D copy of chunk i+1
-  // and the D2H copy of chunk i-1 run on the copy engines while chunk i
-  // computes (the host-pointer call is PCIe-bound: 2.9 GB in / 2.6 GB out per
-  // VGG-19 step against ~29 ms of kernels).  Device pointers: one chunk.
-  const int nchunk = dev ? 1 : std::max(1, std::min(n / 4, 8));
+  // Host pointers: the batch is cut into image chunks that flow through a
+  // three-stage ring (up to 3 device buffers each for x and y): the H2D
+  // stream copies chunk i+1 in while the context stream computes chunk i and
+  // the D2H stream copies chunk i-1 out, so both PCIe directions stay busy
+  // (the host-pointer call is PCIe-bound: 2.9 GB in / 2.6 GB out per VGG-19
+  // step against ~29 ms of kernels).  Events order the reuse of every ring
+  // slot.  Device pointers: one chunk on the context stream.
+  const int nchunk = dev ? 1 : std::max(1, std::min(n / 2, 16));
   const int per = (n + nchunk - 1) / nchunk;
   const size_t x_img = size_t(c) * h * w, y_img = y_elems / size_t(n);
-  const int nbuf = dev ? 0 : std::min(nchunk, 2);
+  const int nbuf = dev ? 0 : std::min(nchunk, 3);
+  const bool piped = nchunk > 1;
   Arena ar{ctx, {}};
-  size_t i_x[2] = {0, 0}, i_y[2] = {0, 0}, i_pix[2] = {0, 0};
+  size_t i_x[3] = {0, 0, 0}, i_y[3] = {0, 0, 0}, i_pix[3] = {0, 0, 0};
   for (int b = 0; b < nbuf; ++b) {
     i_x[b] = ar.add(size_t(per) * x_img * 4);
     i_y[b] = ar.add(size_t(per) * y_img * 4);
@@ -199,9 +202,14 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   auto* dops = reinterpret_cast<unsigned long long*>(p[i_ops]);
   float* wt = (which || ws) ? reinterpret_cast<float*>(p[i_wt]) : nullptr;
   cudaStream_t st = ctx->stream;
-  if (nchunk > 1 && !ctx->aux) {
-    CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&ctx->ev_w, cudaEventDisableTiming));
+  if (piped && !ctx->h2d) {
+    CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    for (int b = 0; b < 3; ++b) {
+      CK(cudaEventCreateWithFlags(&ctx->ev_in[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_comp[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_out[b], cudaEventDisableTiming));
+    }
     CK(cudaEventCreateWithFlags(&ctx->ev_done, cudaEventDisableTiming));
   }
 
@@ -217,27 +225,30 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     TRY(finish_launch(ctx, "transpose_filters_kernel"));
   }
   if (counters) CK(cudaMemsetAsync(dops, 0, 16, st));
-  if (nchunk > 1) {
-    CK(cudaEventRecord(ctx->ev_w, st));
-    CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_w, 0));
+  if (piped) {  // the copy streams start after everything queued so far (ring slots free)
+    CK(cudaEventRecord(ctx->ev_done, st));
+    CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_done, 0));
+    CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_done, 0));
   }
 
-  struct StreamSwap {  // the launch helpers enqueue on ctx->stream
-    sconv_cu_ctx* c;
-    cudaStream_t saved;
-    ~StreamSwap() { c->stream = saved; }
-  } swap{ctx, ctx->stream};
   for (int ci = 0; ci < nchunk; ++ci) {
     const int n0 = ci * per, nb = std::min(per, n - n0);
     if (nb <= 0) break;
-    const int b = ci & 1;
-    ctx->stream = (nchunk > 1 && b) ? ctx->aux : st;
-    cudaStream_t cs = ctx->stream;
+    const int b = dev ? 0 : ci % nbuf;
+    cudaStream_t cs = st;
     const float* dx = dev ? x : reinterpret_cast<float*>(p[i_x[b]]);
     float* dy = dev ? y : reinterpret_cast<float*>(p[i_y[b]]);
-    if (!dev)
+    if (!dev) {
+      cudaStream_t hs = piped ? ctx->h2d : st;
+      if (piped && ci >= nbuf) CK(cudaStreamWaitEvent(hs, ctx->ev_comp[b], 0));  // x slot free
       CK(cudaMemcpyAsync(const_cast<float*>(dx), x + size_t(n0) * x_img, size_t(nb) * x_img * 4,
-                         cudaMemcpyHostToDevice, cs));
+                         cudaMemcpyHostToDevice, hs));
+      if (piped) {
+        CK(cudaEventRecord(ctx->ev_in[b], hs));
+        CK(cudaStreamWaitEvent(cs, ctx->ev_in[b], 0));
+        if (ci >= nbuf) CK(cudaStreamWaitEvent(cs, ctx->ev_out[b], 0));  // y slot drained
+      }
+    }
     if (ws) {
       WsArgs a{dx, wt, dy, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, mode};
       TRY(fast ? launch_ws_fast(ctx, ws, P, a) : launch_ws_exact(ctx, ws, P, a));
@@ -261,8 +272,8 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
         TRY(finish_launch(ctx, "ecr_generic_kernel"));
       }
     }
-    if (counters) {  // integer atomics: order-free across chunks and streams
-      int32_t* pix = reinterpret_cast<int32_t*>(p[i_pix[dev ? 0 : b]]);
+    if (counters) {  // integer atomics: order-free across chunks
+      int32_t* pix = reinterpret_cast<int32_t*>(p[i_pix[b]]);
       pixel_nnz_kernel<<<grid_for(size_t(nb) * h * w, 256, ctx->num_sms), 256, 0, cs>>>(dx, nb, c, h,
                                                                                        w, pix);
       TRY(finish_launch(ctx, "pixel_nnz_kernel"));
@@ -271,13 +282,21 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
       ops_kernel<<<grid_for(items, 256, ctx->num_sms), 256, 0, cs>>>(oa);
       TRY(finish_launch(ctx, "ops_kernel"));
     }
-    if (!dev)
+    if (!dev) {
+      cudaStream_t ds = piped ? ctx->d2h : st;
+      if (piped) {
+        CK(cudaEventRecord(ctx->ev_comp[b], cs));
+        CK(cudaStreamWaitEvent(ds, ctx->ev_comp[b], 0));
+      }
       CK(cudaMemcpyAsync(y + size_t(n0) * y_img, dy, size_t(nb) * y_img * 4, cudaMemcpyDeviceToHost,
-                         cs));
+                         ds));
+      if (piped) CK(cudaEventRecord(ctx->ev_out[b], ds));
+    }
   }
-  ctx->stream = st;
-  if (nchunk > 1) {  // join the second stream back into the context stream
-    CK(cudaEventRecord(ctx->ev_done, ctx->aux));
+  if (piped) {  // join the copy streams back into the context stream
+    CK(cudaEventRecord(ctx->ev_done, ctx->d2h));
+    CK(cudaStreamWaitEvent(st, ctx->ev_done, 0));
+    CK(cudaEventRecord(ctx->ev_done, ctx->h2d));
     CK(cudaStreamWaitEvent(st, ctx->ev_done, 0));
   }
   if (counters) {
@@ -386,12 +405,18 @@ int sconv_cu_ctx_destroy(sconv_cu_ctx* ctx) {
   {
     DeviceGuard guard(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    if (ctx->aux) cudaStreamSynchronize(ctx->aux);
+    if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
+    if (ctx->d2h) cudaStreamSynchronize(ctx->d2h);
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->fwd) cudaFree(ctx->fwd);
     if (ctx->own) cudaStreamDestroy(ctx->own);
-    if (ctx->aux) cudaStreamDestroy(ctx->aux);
-    if (ctx->ev_w) cudaEventDestroy(ctx->ev_w);
+    if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+    if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
+    for (int b = 0; b < 3; ++b) {
+      if (ctx->ev_in[b]) cudaEventDestroy(ctx->ev_in[b]);
+      if (ctx->ev_comp[b]) cudaEventDestroy(ctx->ev_comp[b]);
+      if (ctx->ev_out[b]) cudaEventDestroy(ctx->ev_out[b]);
+    }
     if (ctx->ev_done) cudaEventDestroy(ctx->ev_done);
   }
   delete ctx;
