@@ -49,7 +49,8 @@ struct WsCfg {
   static constexpr int W_STAGE = CC * KK * KT;       // floats
   static constexpr int STAGE = IN_STAGE + W_STAGE;
   static constexpr int NT = 32 * (WPC + 1);          // + producer warp
-  static constexpr int MINB = (NT > 256 || R >= 8) ? 1 : (TH * TW * R <= 32 ? 3 : 2);  // CTAs/SM
+  static constexpr int MINB =  // CTAs/SM (register budget: accumulators + weight registers)
+      (NT > 256 || R >= 8) ? 1 : ((TH * TW * R <= 32 && KH * KW * R <= 36) ? 3 : 2);
   static constexpr int SMEM_BYTES = NS * STAGE * 4 + 2 * NS * 8;
   static constexpr int CELLS = WPC * NPOS;           // input cells per channel
   static constexpr int CELLS_PER_LANE = (CELLS + 31) / 32;

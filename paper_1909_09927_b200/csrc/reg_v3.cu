@@ -5,8 +5,21 @@ namespace sconv_cu {
 namespace host {
 
 // which ws config (0 = none); P is 0 (ECR) or 2 (PECR 2x2/2)
+bool ws_applies(int id, int K, int kh, int kw, int S, int P) {
+  if (S != 1 || !(P == 0 || P == 2) || K < 32) return false;
+  if (id >= 1 && id <= 7) return kh == 3 && kw == 3 && !(id == 2 && P != 0);
+  if (id == 8 || id == 9) return kh == 1 && kw == 1;
+  if (id == 10) return kh == 5 && kw == 5;
+  return false;
+}
+
 int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P) {
-  if (!(kh == 3 && kw == 3 && S == 1 && (P == 0 || P == 2) && K >= 32)) return 0;
+  if (!(S == 1 && (P == 0 || P == 2) && K >= 32)) return 0;
+  // 1x1 / 5x5 (GoogLeNet / LeNet layers, BASELINE config 2): the same
+  // warp-specialised kernel instantiated for that window (tools/config2.py)
+  if (kh == 1 && kw == 1) return K >= 128 ? 8 : 9;
+  if (kh == 5 && kw == 5) return 10;
+  if (!(kh == 3 && kw == 3)) return 0;
   const char* e = std::getenv("SCONV_KERNEL");
   if (e && std::strcmp(e, "v2") == 0) return 0;
   if (e && e[0] == 'w' && e[1] >= 'A' && e[1] <= 'G') return e[1] - 'A' + 1;
@@ -51,6 +64,9 @@ void plan_ws(sconv_launch_plan* out, int ws, int n, int k, int OH, int OW) {
     case 5: plan_ws_t<WsE<0>>(out, ws, n, k, OH, OW); break;
     case 6: plan_ws_t<WsF<0>>(out, ws, n, k, OH, OW); break;
     case 7: plan_ws_t<WsG<0>>(out, ws, n, k, OH, OW); break;
+    case 8: plan_ws_t<WsH<0>>(out, ws, n, k, OH, OW); break;
+    case 9: plan_ws_t<WsI<0>>(out, ws, n, k, OH, OW); break;
+    case 10: plan_ws_t<WsJ<0>>(out, ws, n, k, OH, OW); break;
     default: plan_ws_t<WsC<0>>(out, ws, n, k, OH, OW); break;
   }
 }

@@ -159,13 +159,19 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk);
   int which = (flags & SCONV_F_GENERIC) || ws ? 0 : pick_tiled(k, kh, kw, stride, Pk);
   const bool tileable = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
-  if (forced && tileable && !(flags & SCONV_F_GENERIC)) {
+  if (forced && !(flags & SCONV_F_GENERIC)) {
     if (forced >= 1 && forced <= kNumCfgs) {
-      which = forced;
-      ws = 0;
-    } else if (forced >= 'A' && forced <= 'G' && !(forced == 'B' && Pk != 0)) {
-      ws = forced - 'A' + 1;
-      which = 0;
+      if (tileable) {
+        which = forced;
+        ws = 0;
+      }
+    } else if (forced >= 'A' && forced <= 'J') {
+      if (ws_applies(forced - 'A' + 1, k, kh, kw, stride, Pk)) {
+        ws = forced - 'A' + 1;
+        which = 0;
+      } else {
+        return fail(ctx, SCONV_ERR_ARG, "forced kernel %c does not apply to this shape", forced);
+      }
     } else {
       return fail(ctx, SCONV_ERR_ARG, "unknown forced kernel id %d", forced);
     }
@@ -181,7 +187,36 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   // (the host-pointer call is PCIe-bound: 2.9 GB in / 2.6 GB out per VGG-19
   // step against ~29 ms of kernels).  Events order the reuse of every ring
   // slot.  Device pointers: one chunk on the context stream.
-  const int nchunk = dev ? 1 : std::max(1, std::min(n / 2, 16));
+  static const int chunk_env = [] {  // dev override (tools/e2e_probe.py)
+    const char* e = std::getenv("SCONV_CHUNKS");
+    return e ? std::atoi(e) : 0;
+  }();
+  // Chunk size: small enough to keep both PCIe directions busy, large enough
+  // that one chunk's launch still fills about one wave of CTAs (measured,
+  // tools/e2e_probe.py: conv4_2 loses 20% at 4-image chunks).
+  auto ctas_for = [&](int nb) -> long {
+    sconv_launch_plan pl{};
+    if (ws) {
+      plan_ws(&pl, ws, nb, k, OH, OW);
+      return long(pl.grid_x) * pl.grid_y * pl.grid_z;
+    }
+    if (which) {
+      plan_for(&pl, which, nb, k, OH, OW);
+      return long(pl.grid_x) * pl.grid_y * pl.grid_z;
+    }
+    return long((size_t(nb) * y_elems / std::max(n, 1) + 255) / 256);
+  };
+  int nchunk = 1;
+  if (!dev && n > 1) {
+    if (chunk_env > 0) {
+      nchunk = std::min(n, chunk_env);
+    } else {
+      const long per_img = std::max(1L, ctas_for(n) / n);
+      const long want = 2L * ctx->num_sms;
+      const int imgs_min = static_cast<int>(std::max(2L, (want + per_img - 1) / per_img));
+      nchunk = std::max(1, std::min(32, n / imgs_min));
+    }
+  }
   const int per = (n + nchunk - 1) / nchunk;
   const size_t x_img = size_t(c) * h * w, y_img = y_elems / size_t(n);
   const int nbuf = dev ? 0 : std::min(nchunk, 3);

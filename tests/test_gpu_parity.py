@@ -409,3 +409,43 @@ def test_vgg_full_size_sampled(sc, orc, layer):
             assert close(got, ref)
         else:
             assert bits_equal(got, ref)
+
+
+# ---------------------------------------------------------------------------
+# the v3 kernel instantiated for 1x1 and 5x5 windows (GoogLeNet / LeNet
+# layers of BASELINE config 2), default selection and forced
+# ---------------------------------------------------------------------------
+
+WSHAPES = [
+    # n, c, h, w, k, kh, sparsity
+    (2, 20, 11, 11, 50, 5, 0.95),   # LeNet conv2
+    (2, 32, 14, 14, 128, 5, 0.9),   # GoogLeNet 4e 5x5 branch
+    (2, 48, 12, 13, 96, 5, 0.5),    # ragged tiles
+    (2, 37, 14, 14, 192, 1, 0.9),   # GoogLeNet 4a 1x1 branch
+    (1, 19, 7, 9, 64, 1, 0.7),      # 1x1, K < 128, ragged
+    (1, 8, 10, 10, 256, 1, 0.0),    # 1x1 dense
+]
+
+
+@pytest.mark.parametrize("shape", WSHAPES, ids=[str(s) for s in WSHAPES])
+def test_ws_1x1_5x5(sc, orc, shape):
+    n, c, h, w, k, kk, sp = shape
+    x, f = inputs(orc, n, c, h, w, k, kk, kk, sp, seed=(hash(shape) ^ 91) & 0xFFFF)
+    ref, rops = orc.ecr_conv(x, f, 1)
+    plan = sc.launch_plan(n, c, h, w, k, kk, kk, 1)
+    assert plan["kernel"] == (110 if kk == 5 else (108 if k >= 128 else 109))
+    ops = sc.OpCount()
+    y = sc.ecr_conv_batched(x, f, 1, counters=ops)
+    assert bits_equal(y, ref)
+    assert (ops.multiplications, ops.additions) == rops
+    assert close(sc.ecr_conv_batched(x, f, 1, fast=True), ref)
+    forced = "J" if kk == 5 else ("H" if k >= 128 else "I")
+    assert bits_equal(sc.ecr_conv_batched(x, f, 1, kernel=forced), ref)
+    if (h - kk + 1) % 2 == 0 and (w - kk + 1) % 2 == 0:
+        for mode in (0, 1):
+            pref, _ = orc.pecr_conv(x, f, 1, 2, 2, 2, mode)
+            pool = sc.PoolConfig(2, 2, 2, sc.PoolMode(mode))
+            assert bits_equal(sc.pecr_conv_pool_batched(x, f, 1, pool), pref)
+            assert close(sc.pecr_conv_pool_batched(x, f, 1, pool, fast=True), pref)
+    with pytest.raises(ValueError):  # SCONV_ERR_ARG: a 3x3 config forced on a 1x1/5x5 shape
+        sc.ecr_conv_batched(x, f, 1, kernel="A")
