@@ -122,7 +122,10 @@ def test_launch_plan(sc):
     assert p["grid_x"] == 64 * 7 * 7 // 7 * 4 and p["grid_z"] == 1
     p = sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1)  # 14x14 maps: 2x7 tiles, no waste
     assert p["kernel"] == 102 and p["grid_x"] == 64 * 2 * 4 and p["grid_y"] == 1
-    assert sc.launch_plan(1, 20, 11, 11, 50, 5, 5, 1)["kernel"] == 0
+    # 5x5 / 1x1 windows: the v3 kernel instantiated for them; other shapes: generic
+    assert sc.launch_plan(1, 20, 11, 11, 50, 5, 5, 1)["kernel"] == 110
+    assert sc.launch_plan(1, 480, 14, 14, 192, 1, 1, 1)["kernel"] == 108
+    assert sc.launch_plan(1, 3, 227, 227, 96, 11, 11, 4)["kernel"] == 0
 
 
 def test_value_types(sc):
