@@ -333,6 +333,14 @@ def main():
     achieved_tf = sum(flops) / (sum(layer_ms) * 1e-3) / 1e12
     achieved_gbs = sum(alg_bytes) / (sum(layer_ms) * 1e-3) / 1e9
     dom = max(range(nl), key=lambda l: layer_ms[l])
+    traffic = None  # DRAM bytes of the dominant layer's launch, from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
+            t = json.load(f).get(VGG19[dom][0])
+        if t:
+            traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+    except Exception:
+        pass
 
     # ---- cuDNN dense comparison (same inputs, same GPU) -------------------
     cudnn = {}
@@ -434,7 +442,11 @@ def main():
         "layers_us": {VGG19[l][0]: layer_ms[l] * 1e3 for l in range(nl)},
         "roofline": {
             "bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
-            "frac": achieved_tf / fp32_peak, "traffic": None,
+            "frac": achieved_tf / fp32_peak, "traffic": traffic,
+            "traffic_what": "dram__bytes_read+write of one launch of the dominant layer "
+                            "(profiles/r01/traffic.json) vs its algorithmic bytes "
+                            "dominant_layer_alg_bytes",
+            "dominant_layer_alg_bytes": alg_bytes[dom],
             "what": "useful (nonzero) FLOPs of the fused ECR/PECR kernel over its event time; "
                     "peak = FP32 FFMA 148 SM x 128 x 2 x sm_max_mhz (not in MEASURED_PEAKS)",
             "hbm": {"achieved_gbs": achieved_gbs, "peak_gbs": pk["hbm_gbs"],
