@@ -7,8 +7,11 @@ src/ecr.cpp + src/pecr.cpp, so every ecr_convert / ecr_spmv_conv /
 pecr_convert / pecr_conv_pool call in those tests -- including the ones made
 by multichannel_conv and forward() -- executes on the B200.  The *_ref
 controls are the same programs on the unmodified reference: the drop-in must
-pass exactly what the reference passes (acceptance criterion 8 needs the
-reference CLI, which cannot be built here, in both).
+pass exactly what the reference passes.  The reference CLI
+(proj/tools/sparseconv_main.cpp, against a CLI11 shim) is built both ways too:
+sparseconv_dropin is the CLI backend switch of SURVEY 8f row 2 -- its conv /
+convpool / sweep subcommands run on the B200 -- and the reference's CLI suite
+(cli_main.cpp) and acceptance criterion 8 drive it.
 """
 import os
 import re
@@ -64,5 +67,20 @@ def test_reference_acceptance_on_gpu():
     gpu = _run("acceptance_dropin")
     assert _criteria(gpu.stdout) == _criteria(ref.stdout), gpu.stdout
     crit = _criteria(gpu.stdout)
-    assert len(crit) == 11 and ("FAIL", "8") in crit
-    assert sum(1 for s, _ in crit if s == "PASS") == 10
+    assert len(crit) == 11 and all(s == "PASS" for s, _ in crit), gpu.stdout
+
+
+def test_reference_cli_suite_control():
+    r = _run("cli_ref")
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert re.search(r"\| 0 failed \|", r.stdout)
+
+
+@pytest.mark.gpu
+def test_reference_cli_suite_on_gpu():
+    """The reference CLI built on the drop-in (conv / convpool on the B200)
+    passes the reference's own CLI suite: exit codes, messages, reports,
+    checksums and worker invariance."""
+    r = _run("cli_dropin", {"SCONV_CUDA_MODE": "exact"})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert re.search(r"\| 0 failed \|", r.stdout)
