@@ -6,7 +6,10 @@ namespace host {
 
 // which ws config (0 = none); P is 0 (ECR) or 2 (PECR 2x2/2)
 bool ws_applies(int id, int K, int kh, int kw, int S, int P) {
-  if (S != 1 || !(P == 0 || P == 2) || K < 32) return false;
+  if (!(P == 0 || P == 2) || K < 32) return false;
+  if (id == 11) return kh == 3 && kw == 3 && S == 2;
+  if (id == 12) return kh == 3 && kw == 3 && S == 3;
+  if (S != 1) return false;
   if (id >= 1 && id <= 7) return kh == 3 && kw == 3 && !(id == 2 && P != 0);
   if (id == 8 || id == 9) return kh == 1 && kw == 1;
   if (id == 10) return kh == 5 && kw == 5;
@@ -14,7 +17,11 @@ bool ws_applies(int id, int K, int kh, int kw, int S, int P) {
 }
 
 int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P) {
-  if (!(S == 1 && (P == 0 || P == 2) && K >= 32)) return 0;
+  if (!((P == 0 || P == 2) && K >= 32)) return 0;
+  // strided 3x3 (the paper's stride-2/3 experiments):
+  // 2x2 output tiles whose 5x5 / 6x6 input windows fit the 64-bit mask
+  if (kh == 3 && kw == 3 && (S == 2 || S == 3)) return S == 2 ? 11 : 12;
+  if (S != 1) return 0;
   // 1x1 / 5x5 (GoogLeNet / LeNet layers, BASELINE config 2): the same
   // warp-specialised kernel instantiated for that window (tools/config2.py)
   if (kh == 1 && kw == 1) return K >= 128 ? 8 : 9;
@@ -67,6 +74,8 @@ void plan_ws(sconv_launch_plan* out, int ws, int n, int k, int OH, int OW) {
     case 8: plan_ws_t<WsH<0>>(out, ws, n, k, OH, OW); break;
     case 9: plan_ws_t<WsI<0>>(out, ws, n, k, OH, OW); break;
     case 10: plan_ws_t<WsJ<0>>(out, ws, n, k, OH, OW); break;
+    case 11: plan_ws_t<WsK<0>>(out, ws, n, k, OH, OW); break;
+    case 12: plan_ws_t<WsL<0>>(out, ws, n, k, OH, OW); break;
     default: plan_ws_t<WsC<0>>(out, ws, n, k, OH, OW); break;
   }
 }

@@ -165,7 +165,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
         which = forced;
         ws = 0;
       }
-    } else if (forced >= 'A' && forced <= 'J') {
+    } else if (forced >= 'A' && forced <= 'L') {
       if (ws_applies(forced - 'A' + 1, k, kh, kw, stride, Pk)) {
         ws = forced - 'A' + 1;
         which = 0;

@@ -449,3 +449,36 @@ def test_ws_1x1_5x5(sc, orc, shape):
             assert close(sc.pecr_conv_pool_batched(x, f, 1, pool, fast=True), pref)
     with pytest.raises(ValueError):  # SCONV_ERR_ARG: a 3x3 config forced on a 1x1/5x5 shape
         sc.ecr_conv_batched(x, f, 1, kernel="A")
+
+
+SSHAPES = [
+    # n, c, h, w, k, stride, sparsity
+    (2, 24, 30, 30, 128, 2, 0.7),
+    (2, 16, 31, 29, 160, 2, 0.5),   # ragged tiles, K tail
+    (1, 12, 29, 29, 128, 3, 0.7),
+    (2, 9, 20, 26, 64, 3, 0.9),
+    (1, 8, 17, 17, 256, 2, 0.0),    # dense
+]
+
+
+@pytest.mark.parametrize("shape", SSHAPES, ids=[str(s) for s in SSHAPES])
+def test_ws_strided(sc, orc, shape):
+    n, c, h, w, k, s, sp = shape
+    x, f = inputs(orc, n, c, h, w, k, 3, 3, sp, seed=(hash(shape) ^ 57) & 0xFFFF)
+    ref, rops = orc.ecr_conv(x, f, s)
+    assert sc.launch_plan(n, c, h, w, k, 3, 3, s)["kernel"] == (111 if s == 2 else 112)
+    ops = sc.OpCount()
+    assert bits_equal(sc.ecr_conv_batched(x, f, s, counters=ops), ref)
+    assert (ops.multiplications, ops.additions) == rops
+    assert close(sc.ecr_conv_batched(x, f, s, fast=True), ref)
+    assert bits_equal(sc.ecr_conv_batched(x, f, s, kernel="K" if s == 2 else "L"), ref)
+    try:
+        orc.pack_count(h, 3, s, 2, 2)
+        orc.pack_count(w, 3, s, 2, 2)
+    except Exception:
+        return
+    for mode in (0, 1):
+        pref, _ = orc.pecr_conv(x, f, s, 2, 2, 2, mode)
+        pool = sc.PoolConfig(2, 2, 2, sc.PoolMode(mode))
+        assert bits_equal(sc.pecr_conv_pool_batched(x, f, s, pool), pref)
+        assert close(sc.pecr_conv_pool_batched(x, f, s, pool, fast=True), pref)
