@@ -13,7 +13,8 @@ import os
 from .errors import raise_for
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libsconv_cuda.so")
+# SCONV_LIB: dev override (A/B of build variants, tools/); the default is the in-tree build
+LIB_PATH = os.environ.get("SCONV_LIB") or os.path.join(HERE, "lib", "libsconv_cuda.so")
 
 # exported symbols (kept in sync with include/sconv_cuda.h; tests check both)
 SYMBOLS = (
