@@ -218,6 +218,26 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     }
   }
   const int per = (n + nchunk - 1) / nchunk;
+  // Chunk list: with 4+ chunks the first and last are a quarter size, which
+  // shortens the pipeline fill (first H2D before any compute) and drain (last
+  // compute + D2H after the final H2D) of every synchronous call.
+  std::vector<std::pair<int, int>> chunks;  // (first image, images)
+  {
+    const int edge = nchunk >= 4 ? std::max(1, per / 4) : per;
+    int n0 = 0;
+    if (nchunk >= 4) {
+      chunks.push_back({0, edge});
+      n0 = edge;
+    }
+    const int tail = nchunk >= 4 ? std::min(edge, n - n0) : 0;
+    while (n0 < n - tail) {
+      const int nb = std::min(per, n - tail - n0);
+      chunks.push_back({n0, nb});
+      n0 += nb;
+    }
+    if (tail > 0) chunks.push_back({n0, tail});
+  }
+  nchunk = static_cast<int>(chunks.size());
   const size_t x_img = size_t(c) * h * w, y_img = y_elems / size_t(n);
   const int nbuf = dev ? 0 : std::min(nchunk, 3);
   const bool piped = nchunk > 1;
@@ -267,7 +287,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   }
 
   for (int ci = 0; ci < nchunk; ++ci) {
-    const int n0 = ci * per, nb = std::min(per, n - n0);
+    const int n0 = chunks[ci].first, nb = chunks[ci].second;
     if (nb <= 0) break;
     const int b = dev ? 0 : ci % nbuf;
     cudaStream_t cs = st;
