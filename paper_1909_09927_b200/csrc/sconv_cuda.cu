@@ -20,6 +20,7 @@
 #include "host/internal.h"
 #include "kernels/format.cuh"
 #include "kernels/generic.cuh"
+#include "kernels/smallc.cuh"
 
 using namespace sconv_cu;
 using namespace sconv_cu::host;
@@ -156,10 +157,16 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   if (pecr && pw == ph && pw == ps) P = pw;
   const int Pk = pecr ? (P ? P : -1) : 0;
   const int forced = (flags >> 8) & 0xff;
-  int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk);
-  int which = (flags & SCONV_F_GENERIC) || ws ? 0 : pick_tiled(k, kh, kw, stride, Pk);
+  // few input channels (VGG conv1_1): the per-warp small-C kernel (smallc.cuh)
+  const bool smallc_ok = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
+  bool smallc = !(flags & SCONV_F_GENERIC) && smallc_ok &&
+                (((flags >> 8) & 0xff) == 'M' || (!((flags >> 8) & 0xff) && c <= 4));
+  int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk);
+  int which = (flags & SCONV_F_GENERIC) || ws || smallc ? 0 : pick_tiled(k, kh, kw, stride, Pk);
   const bool tileable = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
-  if (forced && !(flags & SCONV_F_GENERIC)) {
+  if (forced == 'M' && !smallc_ok)
+    return fail(ctx, SCONV_ERR_ARG, "forced kernel M does not apply to this shape");
+  if (forced && forced != 'M' && !(flags & SCONV_F_GENERIC)) {
     if (forced >= 1 && forced <= kNumCfgs) {
       if (tileable) {
         which = forced;
@@ -176,7 +183,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
       return fail(ctx, SCONV_ERR_ARG, "unknown forced kernel id %d", forced);
     }
   }
-  const int Kp = (k + 3) / 4 * 4;
+  const int Kp = smallc ? (k + 63) / 64 * 64 : (k + 3) / 4 * 4;
   const bool counters = muls || adds;
 
   DeviceGuard guard(ctx->device);
@@ -196,6 +203,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   // tools/e2e_probe.py: conv4_2 loses 20% at 4-image chunks).
   auto ctas_for = [&](int nb) -> long {
     sconv_launch_plan pl{};
+    if (smallc) return long((size_t(nb) * ((OH + 3) / 4) * ((OW + 3) / 4) + 7) / 8) * ((k + 63) / 64);
     if (ws) {
       plan_ws(&pl, ws, nb, k, OH, OW);
       return long(pl.grid_x) * pl.grid_y * pl.grid_z;
@@ -248,14 +256,14 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     i_y[b] = ar.add(size_t(per) * y_img * 4);
   }
   const size_t i_w = dev ? 0 : ar.add(w_elems * 4);
-  const size_t i_wt = (which || ws) ? ar.add(size_t(Kp) * c * kh * kw * 4) : 0;
+  const size_t i_wt = (which || ws || smallc) ? ar.add(size_t(Kp) * c * kh * kw * 4) : 0;
   for (int b = 0; b < (counters ? std::max(nbuf, 1) : 0); ++b) i_pix[b] = ar.add(size_t(per) * h * w * 4);
   const size_t i_ops = ar.add(64);
   std::vector<char*> p;
   TRY(ar.commit(p));
   const float* dw = dev ? filt : reinterpret_cast<float*>(p[i_w]);
   auto* dops = reinterpret_cast<unsigned long long*>(p[i_ops]);
-  float* wt = (which || ws) ? reinterpret_cast<float*>(p[i_wt]) : nullptr;
+  float* wt = (which || ws || smallc) ? reinterpret_cast<float*>(p[i_wt]) : nullptr;
   cudaStream_t st = ctx->stream;
   if (piped && !ctx->h2d) {
     CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
@@ -270,7 +278,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
 
   // filters: copy (host path), re-layout for the tiled kernels, once per call
   if (!dev) CK(cudaMemcpyAsync(const_cast<float*>(dw), filt, w_elems * 4, cudaMemcpyHostToDevice, st));
-  if (ws) {
+  if (ws || smallc) {
     transpose_filters_kernel<<<grid_for(size_t(Kp) * c * kh * kw, 256, ctx->num_sms), 256, 0, st>>>(
         dw, wt, k, Kp, c, kh * kw);
     TRY(finish_launch(ctx, "transpose_filters_kernel"));
@@ -304,7 +312,20 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
         if (ci >= nbuf) CK(cudaStreamWaitEvent(cs, ctx->ev_out[b], 0));  // y slot drained
       }
     }
-    if (ws) {
+    if (smallc) {
+      SmallCArgs a{dx, wt, dy, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, mode};
+      a.tiles_x = (OW + 3) / 4;
+      a.tiles_per_img = a.tiles_x * ((OH + 3) / 4);
+      a.total_tiles = a.tiles_per_img * nb;
+      const dim3 grid((a.total_tiles + 7) / 8, (k + 63) / 64);
+      if (P == 2)
+        fast ? ecr_smallc_kernel<2, true><<<grid, 256, 0, cs>>>(a)
+             : ecr_smallc_kernel<2, false><<<grid, 256, 0, cs>>>(a);
+      else
+        fast ? ecr_smallc_kernel<0, true><<<grid, 256, 0, cs>>>(a)
+             : ecr_smallc_kernel<0, false><<<grid, 256, 0, cs>>>(a);
+      TRY(finish_launch(ctx, "ecr_smallc_kernel"));
+    } else if (ws) {
       WsArgs a{dx, wt, dy, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, mode};
       TRY(fast ? launch_ws_fast(ctx, ws, P, a) : launch_ws_exact(ctx, ws, P, a));
     } else if (which) {
@@ -536,9 +557,21 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
     P = (pool_w == pool_h && pool_w == pool_stride) ? pool_w : -1;
   }
   const int forced = (flags >> 8) & 0xff;
-  const int ws = (flags & SCONV_F_GENERIC) ? 0 : pick_ws(k, c, OW, kh, kw, stride, P);
-  const int which = (flags & SCONV_F_GENERIC) || ws ? 0 : pick_tiled(k, kh, kw, stride, P);
-  if (ws) {
+  const bool smallc = !(flags & SCONV_F_GENERIC) && kh == 3 && kw == 3 && stride == 1 &&
+                      (P == 0 || P == 2) && k >= 32 && (forced == 'M' || (!forced && c <= 4));
+  const int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, P);
+  const int which = (flags & SCONV_F_GENERIC) || ws || smallc ? 0 : pick_tiled(k, kh, kw, stride, P);
+  if (smallc) {
+    const long tiles = long(n) * ((OH + 3) / 4) * ((OW + 3) / 4);
+    out->kernel = 300;
+    out->grid_x = static_cast<int>((tiles + 7) / 8);
+    out->grid_y = (k + 63) / 64;
+    out->grid_z = 1;
+    out->block_threads = 256;
+    out->smem_bytes = 8 * 48 * 4;
+    out->tile_h = out->tile_w = 4;
+    out->tile_k = 64;
+  } else if (ws) {
     plan_ws(out, ws, n, k, OH, OW);
   } else if (which) {
     plan_for(out, which, n, k, OH, OW);

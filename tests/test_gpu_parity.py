@@ -482,3 +482,35 @@ def test_ws_strided(sc, orc, shape):
         pool = sc.PoolConfig(2, 2, 2, sc.PoolMode(mode))
         assert bits_equal(sc.pecr_conv_pool_batched(x, f, s, pool), pref)
         assert close(sc.pecr_conv_pool_batched(x, f, s, pool, fast=True), pref)
+
+
+CSHAPES = [
+    # n, c, h, w, k, sparsity
+    (2, 3, 34, 34, 64, 0.7),     # conv1_1-like
+    (3, 1, 19, 23, 96, 0.5),     # ragged tiles, K tail (K-block of 64 half used)
+    (1, 4, 18, 18, 128, 0.0),    # dense, two K-blocks
+    (2, 2, 10, 14, 32, 1.0),     # all zero
+    (2, 3, 66, 34, 128, 0.7),    # 8 tiles per row: shared-memory staged stores, 2 K-blocks
+    (1, 3, 35, 66, 64, 0.6),     # staged stores with a partial last tile row
+]
+
+
+@pytest.mark.parametrize("shape", CSHAPES, ids=[str(s) for s in CSHAPES])
+def test_smallc(sc, orc, shape):
+    n, c, h, w, k, sp = shape
+    x, f = inputs(orc, n, c, h, w, k, 3, 3, sp, seed=(hash(shape) ^ 33) & 0xFFFF)
+    ref, rops = orc.ecr_conv(x, f, 1)
+    assert sc.launch_plan(n, c, h, w, k, 3, 3, 1)["kernel"] == 300
+    ops = sc.OpCount()
+    assert bits_equal(sc.ecr_conv_batched(x, f, 1, counters=ops), ref)
+    assert (ops.multiplications, ops.additions) == rops
+    assert close(sc.ecr_conv_batched(x, f, 1, fast=True), ref)
+    if (h - 2) % 2 == 0 and (w - 2) % 2 == 0:
+        for mode in (0, 1):
+            pref, _ = orc.pecr_conv(x, f, 1, 2, 2, 2, mode)
+            pool = sc.PoolConfig(2, 2, 2, sc.PoolMode(mode))
+            assert bits_equal(sc.pecr_conv_pool_batched(x, f, 1, pool), pref)
+            assert close(sc.pecr_conv_pool_batched(x, f, 1, pool, fast=True), pref)
+    # forced on a wider map ('M')
+    x2, f2 = inputs(orc, 1, 9, 12, 12, 64, 3, 3, 0.6, seed=5)
+    assert bits_equal(sc.ecr_conv_batched(x2, f2, 1, kernel="M"), orc.ecr_conv(x2, f2, 1)[0])

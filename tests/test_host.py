@@ -109,9 +109,9 @@ def test_shard_partition(sc):
 
 
 def test_launch_plan(sc):
-    # few input channels: v2 tiled kernel (Cfg4 for K % 128 != 0)
+    # few input channels (conv1_1): the per-warp small-C kernel, 8 4x4 tiles per CTA
     p = sc.launch_plan(64, 3, 226, 226, 64, 3, 3, 1)
-    assert p["kernel"] == 4 and p["grid_z"] == 64 and p["block_threads"] == 128
+    assert p["kernel"] == 300 and p["grid_x"] == 64 * 56 * 56 // 8 and p["block_threads"] == 256
     # K = 64: v3 with 6x6 tiles (WsG)
     p = sc.launch_plan(64, 64, 226, 226, 64, 3, 3, 1, sc.PoolConfig(2, 2, 2))
     assert p["kernel"] == 107 and p["smem_bytes"] <= 227 * 1024
