@@ -169,6 +169,23 @@ int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h,
                      float* const* conv_outputs, uint64_t* muls,
                      uint64_t* adds, int32_t* pecr_fallback, unsigned flags);
 
+/* ---- feature-map files (src/dataset.cpp:115-247) ------------------------
+ * FMAP ("FMAP", u32le version 1, C, H, W, then LE fp32 values) or CSV by the
+ * path's extension, with the reference's validation: IoError when the file
+ * cannot be opened, FormatError on a bad magic / version / header / dims /
+ * truncated payload / unparsable value.  Host only (no CUDA). */
+const char* sconv_io_last_error(void);
+int sconv_map_file_dims(const char* path, int* c, int* h, int* w);
+/* capacity: floats available at out (ArgError when the map is larger). */
+int sconv_load_map(const char* path, float* out, int64_t capacity, int* c,
+                   int* h, int* w);
+int sconv_save_map(const char* path, const float* values, int c, int h, int w);
+/* N files of identical dims into out[N][C][H][W] (e.g. a pinned buffer for
+ * the batched entries), on `threads` host threads (<= 0: all cores); the
+ * lowest failing file's error is reported, ShapeError when dims differ. */
+int sconv_load_maps(const char* const* paths, int n, float* out, int c, int h,
+                    int w, int threads);
+
 /* ---- formats: the reference's two-phase API (one map, one filter) ------- */
 /* ecr_convert (src/ecr.cpp:51-97) by warp-ballot compaction.  Writes the
  * fixed-slot EcrMap arrays of include/sconv/ecr.hpp:35-45, flattened

@@ -307,6 +307,8 @@ class RefLib(_Lib):
         L.ref_checksum.argtypes = [_f32p, C.c_int64, C.c_char_p]
         L.ref_plan.argtypes = [C.c_int] * 10 + [C.POINTER(C.c_int), C.POINTER(C.c_int), _u64p]
         L.ref_hardware_concurrency.restype = C.c_int
+        L.ref_save_map.argtypes = [C.c_char_p, _f32p, C.c_int, C.c_int, C.c_int]
+        L.ref_load_map.argtypes = [C.c_char_p, _f32p, C.c_int64] + [C.POINTER(C.c_int)] * 3
         L.ref_forward.argtypes = [_f32p] + [C.c_int] * 4 + [C.c_void_p] * 10 + [C.c_int, C.c_int,
                                   _f32p, _f32p, _u64p, _u64p, C.c_void_p]
 
@@ -316,6 +318,17 @@ class RefLib(_Lib):
 
     def hardware_concurrency(self):
         return self.lib.ref_hardware_concurrency()
+
+    def save_map(self, x, path):
+        x = _f32(x)
+        self._chk(self.lib.ref_save_map(str(path).encode(), x.reshape(-1), *x.shape))
+
+    def load_map(self, path, cap=1 << 24):
+        out = np.empty(cap, np.float32)
+        c, h, w = C.c_int(), C.c_int(), C.c_int()
+        self._chk(self.lib.ref_load_map(str(path).encode(), out, cap, C.byref(c), C.byref(h),
+                                        C.byref(w)))
+        return out[:c.value * h.value * w.value].reshape(c.value, h.value, w.value)
 
     def forward(self, x, layers, method, workers=1):
         """sconv::forward (pipeline.cpp:212-301) of the unmodified reference on

@@ -313,6 +313,20 @@ int ref_forward(const float* x, int C, int H, int W, int nl, const int* k, const
   });
 }
 
+// save / load (dataset.cpp:232-243) of the reference, FMAP or CSV by extension.
+int ref_save_map(const char* path, const float* x, int C, int H, int W) {
+  return guarded([&] { save(as_map(x, C, H, W), path); });
+}
+
+int ref_load_map(const char* path, float* out, int64_t cap, int* C, int* H, int* W) {
+  return guarded([&] {
+    const FeatureMap m = load(path);
+    *C = m.channels, *H = m.height, *W = m.width;
+    if (static_cast<int64_t>(m.values.size()) > cap) throw std::runtime_error("capacity");
+    std::memcpy(out, m.values.data(), m.values.size() * sizeof(float));
+  });
+}
+
 int ref_hardware_concurrency() { return static_cast<int>(std::thread::hardware_concurrency()); }
 
 }  // extern "C"

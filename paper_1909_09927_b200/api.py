@@ -822,6 +822,48 @@ def forward(net: NetworkSpec, input: FeatureMap, method: Method,
 # ---------------------------------------------------------------------------
 
 
+def _io_check(st: int) -> None:
+    if st:
+        from .errors import raise_for
+        raise_for(st, nat.lib().sconv_io_last_error().decode())
+
+
+def load(path) -> FeatureMap:
+    """sconv::load (dataset.cpp:240-243): FMAP, or CSV by extension."""
+    L = nat.lib()
+    c, h, w = C.c_int(), C.c_int(), C.c_int()
+    p = str(path).encode()
+    _io_check(L.sconv_map_file_dims(p, C.byref(c), C.byref(h), C.byref(w)))
+    out = np.empty(c.value * h.value * w.value, np.float32)
+    _io_check(L.sconv_load_map(p, _ptr(out), out.size, C.byref(c), C.byref(h), C.byref(w)))
+    return FeatureMap(c.value, h.value, w.value, out)
+
+
+def save(map: FeatureMap, path) -> None:
+    """sconv::save (dataset.cpp:232-238)."""
+    v = np.ascontiguousarray(map.values, np.float32)
+    _io_check(nat.lib().sconv_save_map(str(path).encode(), _ptr(v), map.channels, map.height,
+                                       map.width))
+
+
+def load_batch(paths: Sequence, out=None, threads: int = 0) -> np.ndarray:
+    """N same-dims map files -> [N, C, H, W] (into `out`, e.g. a pinned
+    buffer, when given), read on host threads (sconv_load_maps)."""
+    L = nat.lib()
+    if not paths:
+        raise ConfigError("no files")
+    c, h, w = C.c_int(), C.c_int(), C.c_int()
+    _io_check(L.sconv_map_file_dims(str(paths[0]).encode(), C.byref(c), C.byref(h), C.byref(w)))
+    shape = (len(paths), c.value, h.value, w.value)
+    if out is None:
+        out = np.empty(shape, np.float32)
+    elif tuple(out.shape) != shape or out.dtype != np.float32 or not out.flags.c_contiguous:
+        raise ShapeError("out has the wrong shape")
+    arr = (C.c_char_p * len(paths))(*[str(p).encode() for p in paths])
+    _io_check(L.sconv_load_maps(arr, len(paths), _ptr(out), c.value, h.value, w.value, threads))
+    return out
+
+
 def generate(height: int, width: int, channels: int, sparsity: float, seed: int) -> FeatureMap:
     """sconv::generate (dataset.cpp:77-100), bit-identical."""
     if not (0.0 <= sparsity <= 1.0):
