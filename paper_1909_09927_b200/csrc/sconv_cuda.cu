@@ -225,6 +225,15 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
       nchunk = std::max(1, std::min(32, n / imgs_min));
     }
   }
+  // The kernels index a launch's input and output with 32-bit offsets (the
+  // producer warps keep per-lane int offsets): a launch covers at most 2^30
+  // elements of either, so larger batches are cut into image chunks.
+  {
+    const size_t lim = size_t(1) << 30;
+    const size_t big = std::max(x_elems, y_elems);
+    const int need = static_cast<int>(std::min<size_t>(size_t(n), (big + lim - 1) / lim));
+    nchunk = std::max(nchunk, need);
+  }
   const int per = (n + nchunk - 1) / nchunk;
   // Chunk list: with 4+ chunks the first and last are a quarter size, which
   // shortens the pipeline fill (first H2D before any compute) and drain (last
@@ -248,7 +257,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   nchunk = static_cast<int>(chunks.size());
   const size_t x_img = size_t(c) * h * w, y_img = y_elems / size_t(n);
   const int nbuf = dev ? 0 : std::min(nchunk, 3);
-  const bool piped = nchunk > 1;
+  const bool piped = !dev && nchunk > 1;
   Arena ar{ctx, {}};
   size_t i_x[3] = {0, 0, 0}, i_y[3] = {0, 0, 0}, i_pix[3] = {0, 0, 0};
   for (int b = 0; b < nbuf; ++b) {
@@ -299,8 +308,8 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     if (nb <= 0) break;
     const int b = dev ? 0 : ci % nbuf;
     cudaStream_t cs = st;
-    const float* dx = dev ? x : reinterpret_cast<float*>(p[i_x[b]]);
-    float* dy = dev ? y : reinterpret_cast<float*>(p[i_y[b]]);
+    const float* dx = dev ? x + size_t(n0) * x_img : reinterpret_cast<float*>(p[i_x[b]]);
+    float* dy = dev ? y + size_t(n0) * y_img : reinterpret_cast<float*>(p[i_y[b]]);
     if (!dev) {
       cudaStream_t hs = piped ? ctx->h2d : st;
       if (piped && ci >= nbuf) CK(cudaStreamWaitEvent(hs, ctx->ev_comp[b], 0));  // x slot free

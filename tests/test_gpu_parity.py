@@ -514,3 +514,23 @@ def test_smallc(sc, orc, shape):
     # forced on a wider map ('M')
     x2, f2 = inputs(orc, 1, 9, 12, 12, 64, 3, 3, 0.6, seed=5)
     assert bits_equal(sc.ecr_conv_batched(x2, f2, 1, kernel="M"), orc.ecr_conv(x2, f2, 1)[0])
+
+
+@pytest.mark.slow
+def test_large_batch_chunking(sc):
+    """A device launch whose output exceeds 2^30 elements is cut into image
+    chunks (32-bit in-kernel offsets): results equal per-half launches."""
+    torch = pytest.importorskip("torch")
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    # 33 x 64 x 226^2 inputs (108M) -> 33 x 1024 x 224^2 outputs = 1.7e9 elements (6.8 GB)
+    x = torch.rand(33, 64, 226, 226, device=dev, generator=g)
+    x = x * (torch.rand(x.shape, device=dev, generator=g) >= 0.9)
+    w = torch.rand(1024, 64, 3, 3, device=dev, generator=g) - 0.5
+    y = sc.ecr_conv_batched(x, w, 1, fast=True)
+    for lo, hi in ((0, 1), (16, 17), (32, 33)):
+        ref = sc.ecr_conv_batched(x[lo:hi].contiguous(), w, 1, fast=True)
+        assert torch.equal(y[lo:hi], ref)
+    del y
+    torch.cuda.empty_cache()
