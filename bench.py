@@ -520,11 +520,27 @@ def forward_side(sc, torch, dev, fast, rank):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     nz = float((y != 0).float().mean().item())
+    # batch-1 latency, eager launches vs one CUDA-graph replay (SCONV_F_GRAPH)
+    x1 = x[:1].contiguous()
+    y1 = torch.empty((1,) + tuple(y.shape[1:]), dtype=torch.float32, device=dev)
+    lat = {}
+    for tag, graph in (("eager", False), ("graph", True)):
+        f1 = lambda: sc.forward_batched(x1, layers, sc.Method.kPecr, fast=fast, graph=graph, out=y1)
+        f1()
+        f1()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(10):
+            f1()
+        e1.record()
+        torch.cuda.synchronize()
+        lat[tag] = e0.elapsed_time(e1) / 10
     return {"network": "VGG-19 valid convs (16 conv + ReLU, 5 fused 2x2/2 max pools), input "
                        f"3x{FWD_IN}x{FWD_IN}, batch {FWD_BATCH} per GPU, input sparsity 0.7",
             "ms_per_batch": ms, "images_per_s": FWD_BATCH / (ms * 1e-3),
             "output_shape": list(y.shape), "pecr_fallback_layers": fb,
             "output_nonzero_frac": nz,
+            "batch1_ms": lat,
             "path": "sconv_cu_forward (one call, device pointers)"}
 
 

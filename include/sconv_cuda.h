@@ -61,6 +61,10 @@ typedef enum {
 #define SCONV_F_ASYNC (1u << 2)
 /* Force the generic (one thread per output) kernels; testing only. */
 #define SCONV_F_GENERIC (1u << 3)
+/* sconv_cu_forward only, with SCONV_F_DEVICE and no counters: capture the
+ * network's launches in a CUDA graph on the first call and replay it while
+ * the arguments (pointers, shapes, layers, flags) stay the same. */
+#define SCONV_F_GRAPH (1u << 4)
 /* Force one tiled kernel configuration (testing / tuning only; ignored when
  * the shape is not tileable): 1..6 = v2 TiledCfg1..6, 'A'..'G' = v3 WsA..G.
  * 0 (default) lets the launch layer pick. */

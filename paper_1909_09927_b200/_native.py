@@ -34,6 +34,7 @@ F_FAST = 1 << 0
 F_DEVICE = 1 << 1
 F_ASYNC = 1 << 2
 F_GENERIC = 1 << 3
+F_GRAPH = 1 << 4
 
 
 def F_KERNEL(kid) -> int:

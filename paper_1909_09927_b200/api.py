@@ -693,13 +693,16 @@ def _layer_descs(layers_w, layer_cfg):
 def forward_batched(x, layers: Sequence[dict], method: Method = Method.kPecr, *,
                     fast: bool = False, counters: Optional[OpCount] = None,
                     device: Optional[int] = None, generic: bool = False,
-                    layer_outputs: bool = False, conv_outputs: bool = False, kernel=0):
+                    layer_outputs: bool = False, conv_outputs: bool = False, kernel=0,
+                    graph: bool = False, out=None):
     """forward() of src/pipeline.cpp:212-301 for a batch x [N,C,H,W] with every
     activation resident on the GPU (sconv_cu_forward).  `layers` is a list of
     dicts {"filters": [K,C,kh,kw], "stride": s, "relu": bool, "pool":
     PoolConfig or None}.  numpy in -> numpy out; torch CUDA in -> torch out.
-    Returns (output, layer_outputs list or None, conv_outputs list or None,
-    pecr_fallback_layers)."""
+    `graph` (torch CUDA tensors only): capture the network in a CUDA graph on
+    the first call and replay it while x, out and the layers stay the same
+    (pass the same `out` tensor each time).  Returns (output, layer_outputs
+    list or None, conv_outputs list or None, pecr_fallback_layers)."""
     L = nat.lib()
     if int(method) == Method.kDense:
         raise ConfigError("forward on the GPU runs the compressed methods (ECR, PECR); the dense "
@@ -707,6 +710,8 @@ def forward_batched(x, layers: Sequence[dict], method: Method = Method.kPecr, *,
     flags = (nat.F_FAST if fast else 0) | (nat.F_GENERIC if generic else 0)
     if kernel:
         flags |= nat.F_KERNEL(kernel)
+    if graph:
+        flags |= nat.F_GRAPH
     torch_in = _is_torch_cuda(x)
     if torch_in:
         import torch
@@ -750,7 +755,10 @@ def forward_batched(x, layers: Sequence[dict], method: Method = Method.kPecr, *,
         ctx = nat.context(dev)
         ctx.use_own_stream()
     descs = _layer_descs([ptr(w) for w in ws], cfg)
-    out = mk((N, oc.value, oh.value, ow.value))
+    if out is None:
+        out = mk((N, oc.value, oh.value, ow.value))
+    elif tuple(out.shape) != (N, oc.value, oh.value, ow.value):
+        raise ShapeError("out has the wrong shape")
     lo = [mk((N, k, ph, pw)) for k, _, _, ph, pw in dims] if layer_outputs else None
     fused = [int(method) == Method.kPecr and cf["pool"] is not None and cf["relu"] for cf in cfg]
     co = ([None if fz else mk((N, k, h2, w2)) for fz, (k, h2, w2, _, _) in zip(fused, dims)]

@@ -28,6 +28,9 @@ struct sconv_cu_ctx {
   cudaEvent_t ev_done = nullptr;
   char* fwd = nullptr;              // sconv_cu_forward: resident activations + filters
   size_t fwd_cap = 0;
+  cudaGraphExec_t fwd_graph = nullptr;  // SCONV_F_GRAPH: the captured forward
+  std::string fwd_key;                  // ... and the arguments it was captured for
+  cudaEvent_t ev_graph = nullptr;
 };
 
 namespace sconv_cu {

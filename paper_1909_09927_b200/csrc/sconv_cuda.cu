@@ -494,6 +494,8 @@ int sconv_cu_ctx_destroy(sconv_cu_ctx* ctx) {
     if (ctx->d2h) cudaStreamSynchronize(ctx->d2h);
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->fwd) cudaFree(ctx->fwd);
+    if (ctx->fwd_graph) cudaGraphExecDestroy(ctx->fwd_graph);
+    if (ctx->ev_graph) cudaEventDestroy(ctx->ev_graph);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
@@ -708,15 +710,22 @@ int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int
       off += cnt;
     }
   }
-  const float* cur = x;
+  const float* cur0 = x;
   if (!dev) {
     CK(cudaMemcpyAsync(buf[0], x, size_t(n) * c * h * w * 4, cudaMemcpyHostToDevice, st));
-    cur = buf[0];
+    cur0 = buf[0];
   }
+  if ((flags & SCONV_F_GRAPH) && (!dev || counters))
+    return fail(ctx, SCONV_ERR_ARG, "SCONV_F_GRAPH needs device pointers and no counters");
   const unsigned kflags = (flags & (SCONV_F_FAST | SCONV_F_GENERIC | (0xffu << 8))) | SCONV_F_DEVICE |
                           (counters ? 0u : SCONV_F_ASYNC);
   const cudaMemcpyKind out_kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   uint64_t m_acc = 0, a_acc = 0;
+  // Enqueue every layer on ctx->stream (no host synchronisation unless the
+  // counters are requested), so the whole forward can be captured in a graph.
+  auto enqueue = [&]() -> int {
+  const float* cur = cur0;
+  cudaStream_t st = ctx->stream;
   for (int l = 0; l < nlayers; ++l) {
     const sconv_layer& L = layers[l];
     const FwdLayerDims& d = dims[l];
@@ -763,6 +772,71 @@ int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int
       CK(cudaMemcpyAsync(layer_outputs[l], next, out_elems * 4, out_kind, st));
     if (l == nlayers - 1) CK(cudaMemcpyAsync(y, next, out_elems * 4, out_kind, st));
     cur = next;
+  }
+  return SCONV_OK;
+  };
+
+  if (!(flags & SCONV_F_GRAPH)) {
+    TRY(enqueue());
+  } else {
+    // CUDA graph mode: the first call runs eagerly (sizing every workspace),
+    // then captures the same launch sequence on the context's own stream;
+    // later calls with identical arguments replay the graph (one launch for
+    // the whole network).  The replay is ordered after prior work on the
+    // caller's stream and before anything queued on it afterwards.
+    std::string key(reinterpret_cast<const char*>(&n), sizeof n);
+    auto add = [&](const void* p, size_t b) { key.append(reinterpret_cast<const char*>(p), b); };
+    const void* ptrs[3] = {x, y, reinterpret_cast<const void*>(uintptr_t(method))};
+    add(ptrs, sizeof ptrs);
+    const int dims3[4] = {c, h, w, nlayers};
+    add(dims3, sizeof dims3);
+    add(layers, sizeof(sconv_layer) * nlayers);
+    for (int l = 0; l < nlayers; ++l) {
+      const void* o[2] = {layer_outputs ? layer_outputs[l] : nullptr,
+                          conv_outputs ? conv_outputs[l] : nullptr};
+      add(o, sizeof o);
+    }
+    add(&flags, sizeof flags);
+    if (ctx->fwd_graph && ctx->fwd_key == key) {
+      CK(cudaEventRecord(ctx->ev_graph, st));
+      CK(cudaStreamWaitEvent(ctx->own, ctx->ev_graph, 0));
+      CK(cudaGraphLaunch(ctx->fwd_graph, ctx->own));
+      CK(cudaEventRecord(ctx->ev_graph, ctx->own));
+      CK(cudaStreamWaitEvent(st, ctx->ev_graph, 0));
+      ctx->launches++;
+    } else {
+      TRY(enqueue());  // eager run: produces the result, sizes the workspaces
+      CK(cudaStreamSynchronize(st));
+      if (!ctx->ev_graph) CK(cudaEventCreateWithFlags(&ctx->ev_graph, cudaEventDisableTiming));
+      if (ctx->fwd_graph) {
+        cudaGraphExecDestroy(ctx->fwd_graph);
+        ctx->fwd_graph = nullptr;
+        ctx->fwd_key.clear();
+      }
+      struct StreamSwap {
+        sconv_cu_ctx* c;
+        cudaStream_t saved;
+        ~StreamSwap() { c->stream = saved; }
+      } swap{ctx, ctx->stream};
+      ctx->stream = ctx->own;
+      const uint64_t launches0 = ctx->launches;
+      CK(cudaStreamBeginCapture(ctx->own, cudaStreamCaptureModeThreadLocal));
+      const int rc = enqueue();
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(ctx->own, &graph);
+      ctx->launches = launches0;  // captured, not launched
+      if (rc != SCONV_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+      }
+      if (ec != cudaSuccess) return fail(ctx, SCONV_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ec));
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ei != cudaSuccess) return fail(ctx, SCONV_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ei));
+      ctx->fwd_graph = exec;
+      ctx->fwd_key = key;
+    }
   }
   CK(cudaStreamSynchronize(st));
   if (muls) *muls += m_acc;

@@ -173,3 +173,34 @@ def test_gpu_forward_api(sc, orc, gfwd):
     assert (res.conv_outputs[1].channels, res.conv_outputs[1].height) == (1, 1)  # fused placeholder
     assert res.traffic.device_to_host_bytes == 4 * res.output.size()
     assert res.traffic.host_to_device_bytes == 4 * (x.size + sum(l["filters"].size for l in layers))
+
+
+@pytest.mark.gpu
+def test_gpu_forward_graph_replay(sc, orc):
+    """SCONV_F_GRAPH: the first call runs eagerly and captures; replays give
+    the same bits, follow new input values in the same buffer, and a changed
+    pointer re-captures."""
+    torch = pytest.importorskip("torch")
+    x, layers = batch(orc, NETS["vgg_mini"], 3)
+    dev = torch.device("cuda:0")
+    gl = [dict(l, filters=torch.from_numpy(l["filters"]).to(dev),
+               pool=None if l["pool"] is None else sc.PoolConfig(*l["pool"][:3]))
+          for l in layers]
+    xt = torch.from_numpy(x).to(dev)
+    ref, _, _, _ = sc.forward_batched(xt, gl, sc.Method.kPecr)
+    out = torch.empty_like(ref)
+    for _ in range(3):
+        out.zero_()
+        sc.forward_batched(xt, gl, sc.Method.kPecr, graph=True, out=out)
+        assert torch.equal(out, ref)
+    x2 = np.stack([build(orc, NETS["vgg_mini"], 10 + i)[0] for i in range(3)])
+    xt.copy_(torch.from_numpy(x2))                      # same buffer, new values: replay
+    ref2, _, _, _ = sc.forward_batched(xt.clone(), gl, sc.Method.kPecr)
+    sc.forward_batched(xt, gl, sc.Method.kPecr, graph=True, out=out)
+    assert torch.equal(out, ref2)
+    out2 = torch.empty_like(ref)                        # new output pointer: re-capture
+    sc.forward_batched(xt, gl, sc.Method.kPecr, graph=True, out=out2)
+    assert torch.equal(out2, ref2)
+    with pytest.raises(ValueError):                     # host pointers cannot be captured
+        sc.forward_batched(x, [dict(l, filters=l["filters"].cpu().numpy()) for l in gl],
+                           sc.Method.kPecr, graph=True)
