@@ -277,15 +277,36 @@ def main():
         else:
             sc.ecr_conv_batched(dev_x[l], dev_w[l], 1, fast=fast, out=outs[l], sync=False)
 
-    # correctness spot check vs cuDNN fp32 (not the oracle: full size)
+    # Accuracy spot check at full size (images 0-1 of every layer) against a
+    # float64 convolution: the north-star bar |d| <= 1e-5 + 1e-5|ref| as a
+    # ratio (<= 1 passes) for our output and for cuDNN fp32 (TF32 off).  The
+    # reference's own fp32 sum also deviates from float64 (its order differs),
+    # so the ratio of the oracle itself sits near 1; tests/ pin the oracle.
     max_rel = 0.0
+    acc_ratio = {"ours_vs_reference": 0.0, "cudnn_vs_reference": 0.0, "ours_vs_f64": 0.0,
+                 "cudnn_vs_f64": 0.0}
     for l, (name, C, K, H, pooled) in enumerate(VGG19):
         layer(l)
-        ref = torch.nn.functional.conv2d(dev_x[l][:2], dev_w[l])
+        x2 = dev_x[l][:2]
+        # the reference's own fp32 result: EXACT mode is bit-identical to it
+        # (tests/test_gpu_parity.py, full VGG shapes included)
         if pooled:
-            ref = torch.nn.functional.max_pool2d(torch.relu(ref), 2)
-        got = outs[l][:2]
-        err = ((got - ref).abs() / (1e-3 + ref.abs())).max().item()
+            refx = sc.pecr_conv_pool_batched(x2, dev_w[l], 1, pool_cfg, fast=False)
+        else:
+            refx = sc.ecr_conv_batched(x2, dev_w[l], 1, fast=False)
+        ref64 = torch.nn.functional.conv2d(x2.double(), dev_w[l].double())
+        ref32 = torch.nn.functional.conv2d(x2, dev_w[l])
+        if pooled:
+            ref64 = torch.nn.functional.max_pool2d(torch.relu(ref64), 2)
+            ref32 = torch.nn.functional.max_pool2d(torch.relu(ref32), 2)
+        got, cud, rx = outs[l][:2].double(), ref32.double(), refx.double()
+        for tag, ref in (("reference", rx), ("f64", ref64)):
+            tol = 1e-5 + 1e-5 * ref.abs()
+            acc_ratio["ours_vs_" + tag] = max(acc_ratio["ours_vs_" + tag],
+                                              ((got - ref).abs() / tol).max().item())
+            acc_ratio["cudnn_vs_" + tag] = max(acc_ratio["cudnn_vs_" + tag],
+                                               ((cud - ref).abs() / tol).max().item())
+        err = ((got - cud).abs() / (1e-3 + cud.abs())).max().item()
         max_rel = max(max_rel, err)
     torch.cuda.synchronize()
 
@@ -457,6 +478,10 @@ def main():
         },
         "useful_gflop_per_step": sum(flops) / 1e9,
         "max_rel_err_vs_cudnn": max_rel,
+        "accuracy": {k: round(v, 3) for k, v in acc_ratio.items()},
+        "accuracy_what": "max over all 16 layers (images 0-1) of |out - ref| / (1e-5 + 1e-5|ref|)"
+                         " with ref = the reference's fp32 result (our EXACT mode, bit-identical"
+                         " to it) or a float64 convolution; <= 1 meets the north-star bar",
         "gpu_launches": launches,
         "clocks": clocks,
         "cudnn": cudnn or None,
