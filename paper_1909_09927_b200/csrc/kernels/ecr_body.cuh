@@ -62,6 +62,12 @@ __device__ __forceinline__ void ecr_channel(float (&acc)[TH][TW][R], const float
         if constexpr (!NOSKIP) SCONV_KEEP_BRANCH();
 #elif SCONV_BODY_GUARD == 2
         if constexpr (!NOSKIP) __syncwarp();
+#else
+        // Sparse channels (the ROWSKIP variant) keep every cell behind its
+        // branch: ptxas would otherwise if-convert the 1-3-tap border cells,
+        // whose predicated FFMA2 cost their pipe cycles even when the cell is
+        // zero -- most of a channel's time once density falls below ~0.2.
+        if constexpr (ROWSKIP && !NOSKIP) __syncwarp();
 #endif
         const float v = row[X];
 #pragma unroll
