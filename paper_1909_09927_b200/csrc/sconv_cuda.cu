@@ -219,10 +219,14 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     if (chunk_env > 0) {
       nchunk = std::min(n, chunk_env);
     } else {
-      const long per_img = std::max(1L, ctas_for(n) / n);
-      const long want = 2L * ctx->num_sms;
-      const int imgs_min = static_cast<int>(std::max(2L, (want + per_img - 1) / per_img));
-      nchunk = std::max(1, std::min(32, n / imgs_min));
+      // whole waves: a chunk holds the images whose CTAs fill (just under) one
+      // wave of 2 CTAs per SM, or a multiple of that when there would
+      // otherwise be more than 16 chunks (e.g. conv4_2: 28 CTAs per image ->
+      // 10-image chunks = 0.95 wave; 11 would spill 12 CTAs into a 2nd wave)
+      const double per_img = std::max(1.0, double(ctas_for(n)) / n);
+      const int wave = std::max(1, static_cast<int>(2.0 * ctx->num_sms / per_img));
+      const int chunk = wave * std::max(1, (n + 16 * wave - 1) / (16 * wave));
+      nchunk = std::max(1, (n + chunk - 1) / chunk);
     }
   }
   // The kernels index a launch's input and output with 32-bit offsets (the
