@@ -99,8 +99,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
 // The producer runs ahead and mostly waits for the slowest consumer warp:
 // back off instead of spinning, a polling warp steals issue slots from the
 // consumer warps on its SMSP.
+#ifndef SCONV_PRODUCER_SLEEP_NS
+#define SCONV_PRODUCER_SLEEP_NS 256
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
-  while (!mbar_try_wait(b, parity)) __nanosleep(256);
+  while (!mbar_try_wait(b, parity)) __nanosleep(SCONV_PRODUCER_SLEEP_NS);
 }
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, unsigned bytes) {
