@@ -87,6 +87,29 @@ __global__ void transpose_filters_kernel(const float* __restrict__ w, float* __r
   }
 }
 
+// PECR pooling of a conv output already in memory (pecr_conv_pool's fold,
+// src/pecr.cpp:147-167: windows n = 0 .. pw*ph-1 in raster order, max from
+// +0.0 -> ReLU folded, or mean of max(acc, 0)).  Used for pool shapes the
+// fused epilogue does not cover (anything but 2x2/2): conv by a tiled kernel,
+// then this -- bit-identical to the fused / generic PECR in EXACT mode.
+__global__ void pecr_pool_fold_kernel(const float* __restrict__ conv, float* __restrict__ y,
+                                      size_t planes, int OH, int OW, int pw, int ph, int ps,
+                                      int mode, int PH, int PW) {
+  const size_t total = planes * PH * PW;
+  const int wpp = pw * ph;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(idx % PW);
+    const int b = static_cast<int>((idx / PW) % PH);
+    const size_t pl = idx / (static_cast<size_t>(PW) * PH);
+    const float* cp = conv + pl * OH * OW;
+    PoolFold f;
+    for (int q = 0; q < wpp; ++q)
+      f.add(cp[static_cast<size_t>(b * ps + q / pw) * OW + t * ps + q % pw], mode);
+    y[idx] = f.result(mode, wpp);
+  }
+}
+
 // ReLU in place (Activation::kRelu after an unfused conv).
 __global__ void relu_kernel(float* __restrict__ v, size_t n) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;

@@ -163,6 +163,17 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
                 (((flags >> 8) & 0xff) == 'M' || (!((flags >> 8) & 0xff) && c <= 4));
   int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk);
   int which = (flags & SCONV_F_GENERIC) || ws || smallc ? 0 : pick_tiled(k, kh, kw, stride, Pk);
+  // PECR with a pool the fused epilogue does not cover (anything but 2x2/2):
+  // a tiled kernel computes the conv into a workspace, then
+  // pecr_pool_fold_kernel folds the pools (the pre-pool map does reach HBM).
+  bool pool_after = false;
+  if (pecr && Pk != 2 && !ws && !which && !smallc && !(flags & SCONV_F_GENERIC) &&
+      !((flags >> 8) & 0xff)) {
+    smallc = kh == 3 && kw == 3 && stride == 1 && k >= 32 && c <= 4;
+    ws = smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0);
+    which = smallc || ws ? 0 : pick_tiled(k, kh, kw, stride, 0);
+    pool_after = smallc || ws || which;
+  }
   const bool tileable = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
   if (forced == 'M' && !smallc_ok)
     return fail(ctx, SCONV_ERR_ARG, "forced kernel M does not apply to this shape");
@@ -271,6 +282,8 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   const size_t i_w = dev ? 0 : ar.add(w_elems * 4);
   const size_t i_wt = (which || ws || smallc) ? ar.add(size_t(Kp) * c * kh * kw * 4) : 0;
   for (int b = 0; b < (counters ? std::max(nbuf, 1) : 0); ++b) i_pix[b] = ar.add(size_t(per) * h * w * 4);
+  const size_t conv_img = size_t(k) * OH * OW;
+  const size_t i_conv = pool_after ? ar.add(size_t(per) * conv_img * 4) : 0;
   const size_t i_ops = ar.add(64);
   std::vector<char*> p;
   TRY(ar.commit(p));
@@ -314,6 +327,9 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     cudaStream_t cs = st;
     const float* dx = dev ? x + size_t(n0) * x_img : reinterpret_cast<float*>(p[i_x[b]]);
     float* dy = dev ? y + size_t(n0) * y_img : reinterpret_cast<float*>(p[i_y[b]]);
+    float* dconv = pool_after ? reinterpret_cast<float*>(p[i_conv]) : dy;  // conv kernels write here
+    const int Pl = pool_after ? 0 : P;
+    const int model = pool_after ? 0 : mode;
     if (!dev) {
       cudaStream_t hs = piped ? ctx->h2d : st;
       if (piped && ci >= nbuf) CK(cudaStreamWaitEvent(hs, ctx->ev_comp[b], 0));  // x slot free
@@ -326,12 +342,12 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
       }
     }
     if (smallc) {
-      SmallCArgs a{dx, wt, dy, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, mode};
+      SmallCArgs a{dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, model};
       a.tiles_x = (OW + 3) / 4;
       a.tiles_per_img = a.tiles_x * ((OH + 3) / 4);
       a.total_tiles = a.tiles_per_img * nb;
       const dim3 grid((a.total_tiles + 7) / 8, (k + 63) / 64);
-      if (P == 2)
+      if (Pl == 2)
         fast ? ecr_smallc_kernel<2, true><<<grid, 256, 0, cs>>>(a)
              : ecr_smallc_kernel<2, false><<<grid, 256, 0, cs>>>(a);
       else
@@ -339,11 +355,11 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
              : ecr_smallc_kernel<0, false><<<grid, 256, 0, cs>>>(a);
       TRY(finish_launch(ctx, "ecr_smallc_kernel"));
     } else if (ws) {
-      WsArgs a{dx, wt, dy, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, mode};
-      TRY(fast ? launch_ws_fast(ctx, ws, P, a) : launch_ws_exact(ctx, ws, P, a));
+      WsArgs a{dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, model};
+      TRY(fast ? launch_ws_fast(ctx, ws, Pl, a) : launch_ws_exact(ctx, ws, Pl, a));
     } else if (which) {
-      TiledArgs a{dx, wt, dy, c, h, w, k, OH, OW, 0, mode};
-      TRY(launch_tiled(ctx, fast, which, P, a, nb));
+      TiledArgs a{dx, wt, dconv, c, h, w, k, OH, OW, 0, model};
+      TRY(launch_tiled(ctx, fast, which, Pl, a, nb));
     } else {
       GenericArgs a{dx, dw, dy, nb, c, h, w, k, kh, kw, stride, OH, OW, pw, ph, ps, mode, PHo, PWo};
       const unsigned g = grid_for(size_t(nb) * y_img, 256, ctx->num_sms);
@@ -360,6 +376,12 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
           ecr_generic_kernel<false><<<g, 256, 0, cs>>>(a);
         TRY(finish_launch(ctx, "ecr_generic_kernel"));
       }
+    }
+    if (pool_after) {
+      const size_t planes = size_t(nb) * k;
+      pecr_pool_fold_kernel<<<grid_for(planes * PHo * PWo, 256, ctx->num_sms), 256, 0, cs>>>(
+          dconv, dy, planes, OH, OW, pw, ph, ps, mode, PHo, PWo);
+      TRY(finish_launch(ctx, "pecr_pool_fold_kernel"));
     }
     if (counters) {  // integer atomics: order-free across chunks
       int32_t* pix = reinterpret_cast<int32_t*>(p[i_pix[b]]);
@@ -572,10 +594,16 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
     P = (pool_w == pool_h && pool_w == pool_stride) ? pool_w : -1;
   }
   const int forced = (flags >> 8) & 0xff;
-  const bool smallc = !(flags & SCONV_F_GENERIC) && kh == 3 && kw == 3 && stride == 1 &&
-                      (P == 0 || P == 2) && k >= 32 && (forced == 'M' || (!forced && c <= 4));
-  const int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, P);
-  const int which = (flags & SCONV_F_GENERIC) || ws || smallc ? 0 : pick_tiled(k, kh, kw, stride, P);
+  bool smallc = !(flags & SCONV_F_GENERIC) && kh == 3 && kw == 3 && stride == 1 &&
+                (P == 0 || P == 2) && k >= 32 && (forced == 'M' || (!forced && c <= 4));
+  int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, P);
+  int which = (flags & SCONV_F_GENERIC) || ws || smallc ? 0 : pick_tiled(k, kh, kw, stride, P);
+  if (pool_w > 0 && P != 2 && !ws && !which && !smallc && !(flags & SCONV_F_GENERIC) && !forced) {
+    // conv by a tiled kernel, then pecr_pool_fold_kernel (see fused_conv)
+    smallc = kh == 3 && kw == 3 && stride == 1 && k >= 32 && c <= 4;
+    ws = smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0);
+    which = smallc || ws ? 0 : pick_tiled(k, kh, kw, stride, 0);
+  }
   if (smallc) {
     const long tiles = long(n) * ((OH + 3) / 4) * ((OW + 3) / 4);
     out->kernel = 300;

@@ -534,3 +534,28 @@ def test_large_batch_chunking(sc):
         assert torch.equal(y[lo:hi], ref)
     del y
     torch.cuda.empty_cache()
+
+
+PSHAPES = [
+    # n, c, h, w, k, kh, stride, (pw, ph, ps), sparsity
+    (2, 16, 17, 17, 64, 3, 1, (3, 3, 2), 0.7),    # overlapping 3x3/2 (AlexNet-style)
+    (1, 24, 14, 20, 128, 3, 1, (2, 3, 1), 0.5),   # non-square, stride 1
+    (2, 3, 20, 20, 64, 3, 1, (3, 3, 3), 0.7),     # small C (smallc conv), 3x3/3
+    (1, 20, 15, 15, 48, 5, 1, (3, 3, 2), 0.8),    # 5x5 conv, overlapping pool
+]
+
+
+@pytest.mark.parametrize("shape", PSHAPES, ids=[str(s) for s in PSHAPES])
+def test_pecr_other_pools(sc, orc, shape):
+    """Pools other than 2x2/2: conv by a tiled kernel, then the PECR fold --
+    bit-identical to the reference's pecr_conv_pool in EXACT mode."""
+    n, c, h, w, k, kk, s, (pw, ph, ps), sp = shape
+    x, f = inputs(orc, n, c, h, w, k, kk, kk, sp, seed=(hash(shape) ^ 21) & 0xFFFF)
+    assert sc.launch_plan(n, c, h, w, k, kk, kk, s, sc.PoolConfig(pw, ph, ps))["kernel"] != 0
+    for mode in (0, 1):
+        pref, rops = orc.pecr_conv(x, f, s, pw, ph, ps, mode)
+        pool = sc.PoolConfig(pw, ph, ps, sc.PoolMode(mode))
+        ops = sc.OpCount()
+        assert bits_equal(sc.pecr_conv_pool_batched(x, f, s, pool, counters=ops), pref)
+        assert (ops.multiplications, ops.additions) == rops
+        assert close(sc.pecr_conv_pool_batched(x, f, s, pool, fast=True), pref)
