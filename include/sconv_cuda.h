@@ -56,8 +56,12 @@ typedef enum {
 /* Every tensor pointer is a device pointer on the context's device (no
  * host<->device copies).  Without it all pointers are host pointers. */
 #define SCONV_F_DEVICE (1u << 1)
-/* With SCONV_F_DEVICE: return right after enqueueing on the context stream
- * (no stream synchronisation).  Counters must then be NULL. */
+/* Return right after enqueueing (no synchronisation); counters must be NULL.
+ * With SCONV_F_DEVICE the work is ordered on the context stream.  With host
+ * pointers the call owns one of 16 rotating workspaces and its own
+ * H2D / compute / D2H ring, so consecutive calls overlap their transfers;
+ * the inputs must stay unchanged and the outputs unread until
+ * sconv_cu_synchronize(ctx) (use pinned memory for the copies to overlap). */
 #define SCONV_F_ASYNC (1u << 2)
 /* Force the generic (one thread per output) kernels; testing only. */
 #define SCONV_F_GENERIC (1u << 3)

@@ -154,6 +154,13 @@ class Context:
 
     def synchronize(self) -> None:
         check(lib().sconv_cu_synchronize(self.handle), self.handle)
+        self._inflight = []
+
+    def keep(self, *arrays) -> None:
+        """Hold host buffers of asynchronous calls until synchronize()."""
+        if not hasattr(self, "_inflight"):
+            self._inflight = []
+        self._inflight.extend(arrays)
 
     @property
     def launches(self) -> int:

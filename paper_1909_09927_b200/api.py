@@ -524,6 +524,12 @@ def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, co
             out = np.empty(shape, np.float32)
         ctx = nat.context(0 if device is None else device)
         ctx.use_own_stream()
+        if not sync and counters is None:
+            # asynchronous host-pointer call: the buffers must outlive it
+            if not (out.flags.c_contiguous and out.dtype == np.float32):
+                raise ShapeError("async calls need a C-contiguous float32 out")
+            flags |= nat.F_ASYNC
+            ctx.keep(x, filters, out)
         xp, wp, yp = _ptr(x), _ptr(filters), _ptr(out)
     m, a = C.c_uint64(0), C.c_uint64(0)
     mp = C.byref(m) if counters is not None else None
@@ -540,6 +546,12 @@ def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, co
     return out
 
 
+def synchronize(device: int = 0) -> None:
+    """Wait for every call enqueued on `device`'s context (sconv_cu_synchronize);
+    host buffers of asynchronous (sync=False) numpy calls are valid after it."""
+    nat.context(device).synchronize()
+
+
 def ecr_conv_batched(x, filters, stride: int = 1, *, fast: bool = False,
                      counters: Optional[OpCount] = None, device: Optional[int] = None,
                      generic: bool = False, out=None, sync: bool = True, kernel=0):
@@ -547,7 +559,9 @@ def ecr_conv_batched(x, filters, stride: int = 1, *, fast: bool = False,
 
     Equivalent to multichannel_conv(map, filters, {stride}, Method::kEcr) per
     image (pipeline.cpp:191-210).  numpy in -> numpy out (host copies inside);
-    torch CUDA tensors in -> torch out on the current stream.  `kernel`
+    torch CUDA tensors in -> torch out on the current stream.  sync=False
+    returns after enqueueing (numpy: pinned buffers overlap; call
+    synchronize() before reading out).  `kernel`
     forces a tiled configuration (testing / tuning; SCONV_F_KERNEL).
     """
     return _batched("ecr", x, filters, stride, None, 0, fast, counters, device, generic, out,

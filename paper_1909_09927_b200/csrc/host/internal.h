@@ -22,6 +22,17 @@ struct sconv_cu_ctx {
   size_t ws_cap = 0;
   int num_sms = 148;
   int smem_optin = 0;
+  // Workspaces of asynchronous host-pointer calls (SCONV_F_ASYNC without
+  // SCONV_F_DEVICE): a call in flight owns one of these until its last D2H
+  // (ev_hws) -- the rotation lets the H2D of the next call overlap the
+  // compute / D2H of the previous ones.
+  static constexpr int kHostArenas = 16;  // capacity; hws_n are used
+  int hws_n = 6;
+  size_t hws_max = 0;  // largest host workspace so far: a growing one jumps to it
+  char* hws[kHostArenas] = {};
+  size_t hws_cap[kHostArenas] = {};
+  cudaEvent_t ev_hws[kHostArenas] = {};
+  int hws_next = 0;
   // host-pointer pipeline: copy streams and per-buffer events (fused_conv)
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_in[3] = {}, ev_comp[3] = {}, ev_out[3] = {};

@@ -76,6 +76,8 @@ struct DeviceGuard {
 struct Arena {
   sconv_cu_ctx* ctx;
   std::vector<size_t> sizes;
+  int host = -1;  // >= 0: one of the async host-call workspaces (ctx->hws[host])
+  bool grew = false;  // a host workspace was (re)allocated on ctx->stream
   size_t add(size_t bytes) {
     sizes.push_back((bytes + 255) & ~size_t{255});
     return sizes.size() - 1;
@@ -83,19 +85,34 @@ struct Arena {
   int commit(std::vector<char*>& out) {
     size_t total = 0;
     for (size_t s : sizes) total += s;
-    if (total > ctx->ws_cap) {
-      const size_t cap = std::max(total, ctx->ws_cap + ctx->ws_cap / 2);
-      CK(cudaStreamSynchronize(ctx->stream));
-      if (ctx->ws) CK(cudaFree(ctx->ws));
-      ctx->ws = nullptr;
-      ctx->ws_cap = 0;
-      CK(cudaMalloc(&ctx->ws, cap));
-      ctx->ws_cap = cap;
+    char*& base = host >= 0 ? ctx->hws[host] : ctx->ws;
+    size_t& cap_ = host >= 0 ? ctx->hws_cap[host] : ctx->ws_cap;
+    if (total > cap_) {
+      size_t cap = std::max(total, cap_ + cap_ / 2);
+      if (host >= 0) cap = ctx->hws_max = std::max(ctx->hws_max, cap);
+      // queued work may still read the old buffer (a host workspace is idle:
+      // its previous call was waited for before this one took it)
+      if (host < 0) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (base) CK(cudaFree(base));
+        base = nullptr;
+        cap_ = 0;
+        CK(cudaMalloc(&base, cap));
+      } else {
+        // stream-ordered: no device-wide synchronisation (cudaFree would
+        // stall every call in flight)
+        if (base) CK(cudaFreeAsync(base, ctx->stream));
+        base = nullptr;
+        cap_ = 0;
+        CK(cudaMallocAsync(&base, cap, ctx->stream));
+        grew = true;
+      }
+      cap_ = cap;
     }
     out.clear();
     size_t off = 0;
     for (size_t s : sizes) {
-      out.push_back(ctx->ws + off);
+      out.push_back(base + off);
       off += s;
     }
     return SCONV_OK;
@@ -146,8 +163,11 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     TRY(pack_count(ctx, h, kh, stride, ph, ps, &PHo));
   }
   const bool dev = flags & SCONV_F_DEVICE, async = flags & SCONV_F_ASYNC, fast = flags & SCONV_F_FAST;
-  if (async && !dev) return fail(ctx, SCONV_ERR_ARG, "SCONV_F_ASYNC requires SCONV_F_DEVICE");
   if (async && (muls || adds)) return fail(ctx, SCONV_ERR_ARG, "counters need a synchronous call");
+  // async host pointers: the call returns after enqueueing; x must stay
+  // unchanged and y unread until sconv_cu_synchronize (pinned memory for
+  // the copies to overlap).
+  const bool host_async = async && !dev;
   if (n == 0 || k == 0) return SCONV_OK;
   if (!x || !filt || !y) return fail(ctx, SCONV_ERR_ARG, "null tensor pointer");
 
@@ -274,6 +294,12 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   const int nbuf = dev ? 0 : std::min(nchunk, 3);
   const bool piped = !dev && nchunk > 1;
   Arena ar{ctx, {}};
+  if (host_async) {  // take the next host workspace once its previous call is done
+    ar.host = ctx->hws_next;
+    ctx->hws_next = (ctx->hws_next + 1) % ctx->hws_n;
+    if (!ctx->ev_hws[ar.host]) CK(cudaEventCreateWithFlags(&ctx->ev_hws[ar.host], cudaEventDisableTiming));
+    else CK(cudaEventSynchronize(ctx->ev_hws[ar.host]));
+  }
   size_t i_x[3] = {0, 0, 0}, i_y[3] = {0, 0, 0}, i_pix[3] = {0, 0, 0};
   for (int b = 0; b < nbuf; ++b) {
     i_x[b] = ar.add(size_t(per) * x_img * 4);
@@ -302,8 +328,25 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     CK(cudaEventCreateWithFlags(&ctx->ev_done, cudaEventDisableTiming));
   }
 
-  // filters: copy (host path), re-layout for the tiled kernels, once per call
-  if (!dev) CK(cudaMemcpyAsync(const_cast<float*>(dw), filt, w_elems * 4, cudaMemcpyHostToDevice, st));
+  if (piped && host_async && ar.grew) {  // the new workspace exists in ctx->stream order
+    CK(cudaEventRecord(ctx->ev_done, st));
+    CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_done, 0));
+    CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_done, 0));
+  }
+  // filters: copy (host path), re-layout for the tiled kernels, once per call.
+  // Async host calls send them on the H2D stream, ahead of this call's input
+  // chunks: issued on the context stream they would queue behind every input
+  // copy already submitted to the H2D engine (the previous calls' inputs).
+  if (!dev) {
+    if (host_async && piped) {
+      CK(cudaMemcpyAsync(const_cast<float*>(dw), filt, w_elems * 4, cudaMemcpyHostToDevice,
+                         ctx->h2d));
+      CK(cudaEventRecord(ctx->ev_done, ctx->h2d));
+      CK(cudaStreamWaitEvent(st, ctx->ev_done, 0));
+    } else {
+      CK(cudaMemcpyAsync(const_cast<float*>(dw), filt, w_elems * 4, cudaMemcpyHostToDevice, st));
+    }
+  }
   if (ws || smallc) {
     transpose_filters_kernel<<<grid_for(size_t(Kp) * c * kh * kw, 256, ctx->num_sms), 256, 0, st>>>(
         dw, wt, k, Kp, c, kh * kw);
@@ -314,11 +357,13 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     TRY(finish_launch(ctx, "transpose_filters_kernel"));
   }
   if (counters) CK(cudaMemsetAsync(dops, 0, 16, st));
-  if (piped) {  // the copy streams start after everything queued so far (ring slots free)
+  if (piped && !host_async) {  // the copy streams start after everything queued so far
     CK(cudaEventRecord(ctx->ev_done, st));
     CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_done, 0));
     CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_done, 0));
   }
+  // (async host calls own fresh ring slots: their first H2D copies need not
+  // wait for the previous call's compute or D2H)
 
   for (int ci = 0; ci < nchunk; ++ci) {
     const int n0 = chunks[ci].first, nb = chunks[ci].second;
@@ -404,7 +449,16 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
       if (piped) CK(cudaEventRecord(ctx->ev_out[b], ds));
     }
   }
-  if (piped) {  // join the copy streams back into the context stream
+  if (host_async) {
+    // the workspace is free once the last D2H (which follows the last kernel)
+    // and the whole of the context stream's work for this call are done
+    cudaStream_t ds = piped ? ctx->d2h : st;
+    if (piped) {
+      CK(cudaEventRecord(ctx->ev_done, st));
+      CK(cudaStreamWaitEvent(ds, ctx->ev_done, 0));
+    }
+    CK(cudaEventRecord(ctx->ev_hws[ar.host], ds));
+  } else if (piped) {  // join the copy streams back into the context stream
     CK(cudaEventRecord(ctx->ev_done, ctx->d2h));
     CK(cudaStreamWaitEvent(st, ctx->ev_done, 0));
     CK(cudaEventRecord(ctx->ev_done, ctx->h2d));
@@ -499,6 +553,14 @@ int sconv_cu_ctx_create(int device, sconv_cu_ctx** out) {
   ctx = new sconv_cu_ctx();
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
+  {  // async host-call workspaces come from the device's default memory pool:
+     // keep freed blocks mapped instead of trimming them at every sync point
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   ctx->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
   DeviceGuard guard(device);
   e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
@@ -507,6 +569,8 @@ int sconv_cu_ctx_create(int device, sconv_cu_ctx** out) {
     return fail(nullptr, SCONV_ERR_CUDA, "%s", cudaGetErrorString(e));
   }
   ctx->stream = ctx->own;
+  if (const char* e = std::getenv("SCONV_HOST_ARENAS"))  // dev knob (tools/async_probe.py)
+    ctx->hws_n = std::max(1, std::min(sconv_cu_ctx::kHostArenas, std::atoi(e)));
   *out = ctx;
   return SCONV_OK;
 }
@@ -519,6 +583,12 @@ int sconv_cu_ctx_destroy(sconv_cu_ctx* ctx) {
     if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
     if (ctx->d2h) cudaStreamSynchronize(ctx->d2h);
     if (ctx->ws) cudaFree(ctx->ws);
+    for (int a = 0; a < sconv_cu_ctx::kHostArenas; ++a) {
+      if (ctx->ev_hws[a]) cudaEventSynchronize(ctx->ev_hws[a]);
+      if (ctx->hws[a]) cudaFreeAsync(ctx->hws[a], ctx->stream);
+      if (ctx->ev_hws[a]) cudaEventDestroy(ctx->ev_hws[a]);
+    }
+    cudaStreamSynchronize(ctx->stream);
     if (ctx->fwd) cudaFree(ctx->fwd);
     if (ctx->fwd_graph) cudaGraphExecDestroy(ctx->fwd_graph);
     if (ctx->ev_graph) cudaEventDestroy(ctx->ev_graph);
@@ -559,6 +629,8 @@ int sconv_cu_synchronize(sconv_cu_ctx* ctx) {
   if (!ctx) return SCONV_ERR_ARG;
   DeviceGuard guard(ctx->device);
   CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->h2d) CK(cudaStreamSynchronize(ctx->h2d));  // async host-pointer calls
+  if (ctx->d2h) CK(cudaStreamSynchronize(ctx->d2h));
   return SCONV_OK;
 }
 

@@ -559,3 +559,36 @@ def test_pecr_other_pools(sc, orc, shape):
         assert bits_equal(sc.pecr_conv_pool_batched(x, f, s, pool, counters=ops), pref)
         assert (ops.multiplications, ops.additions) == rops
         assert close(sc.pecr_conv_pool_batched(x, f, s, pool, fast=True), pref)
+
+
+def test_async_host_calls(sc, orc):
+    """SCONV_F_ASYNC with host pointers: several layers enqueued back to back
+    (rotating workspaces, overlapping transfers) equal the synchronous calls
+    once synchronize() returns."""
+    torch = pytest.importorskip("torch")
+    shapes = [(9, 8, 18, 18, 64, 0), (9, 64, 18, 18, 128, 2), (9, 16, 12, 12, 256, 0),
+              (12, 3, 34, 34, 64, 0), (9, 32, 10, 10, 128, 2)]
+    xs, ws, want, outs = [], [], [], []
+    for i, (n, c, h, w, k, pool) in enumerate(shapes):
+        x, f = inputs(orc, n, c, h, w, k, 3, 3, 0.7, seed=300 + i)
+        x = torch.from_numpy(x).pin_memory().numpy()
+        f = torch.from_numpy(f).pin_memory().numpy()
+        if pool:
+            ref = sc.pecr_conv_pool_batched(x, f, 1, sc.PoolConfig(2, 2, 2), fast=True)
+        else:
+            ref = sc.ecr_conv_batched(x, f, 1, fast=True)
+        xs.append(x)
+        ws.append(f)
+        want.append(ref)
+        outs.append(torch.empty(ref.shape, dtype=torch.float32).pin_memory().numpy())
+    for rep in range(2):
+        for (n, c, h, w, k, pool), x, f, o in zip(shapes, xs, ws, outs):
+            o.fill(-1.0)
+            if pool:
+                sc.pecr_conv_pool_batched(x, f, 1, sc.PoolConfig(2, 2, 2), fast=True, out=o,
+                                          sync=False)
+            else:
+                sc.ecr_conv_batched(x, f, 1, fast=True, out=o, sync=False)
+        sc.synchronize()
+        for o, r in zip(outs, want):
+            assert bits_equal(o, r)
