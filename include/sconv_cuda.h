@@ -177,6 +177,15 @@ int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h,
                      float* const* conv_outputs, uint64_t* muls,
                      uint64_t* adds, int32_t* pecr_fallback, unsigned flags);
 
+/* ---- sparsity profiling (src/dataset.cpp:249-286) ----------------------
+ * window_nnz_counts for N maps: counts[N][oh][ow] (NULL: not written) = the
+ * nonzeros of every conv window over all channels; raw[N] / extended[N]
+ * (NULL: not written) = sparsity_profile's zero fraction of the map and of
+ * its im2col extension.  Integer counts, exact ratios. */
+int sconv_cu_window_nnz(sconv_cu_ctx* ctx, const float* x, int n, int c, int h,
+                        int w, int kh, int kw, int stride, int32_t* counts,
+                        double* raw, double* extended, unsigned flags);
+
 /* ---- feature-map files (src/dataset.cpp:115-247) ------------------------
  * FMAP ("FMAP", u32le version 1, C, H, W, then LE fp32 values) or CSV by the
  * path's extension, with the reference's validation: IoError when the file

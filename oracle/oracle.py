@@ -307,6 +307,7 @@ class RefLib(_Lib):
         L.ref_checksum.argtypes = [_f32p, C.c_int64, C.c_char_p]
         L.ref_plan.argtypes = [C.c_int] * 10 + [C.POINTER(C.c_int), C.POINTER(C.c_int), _u64p]
         L.ref_hardware_concurrency.restype = C.c_int
+        L.ref_sparsity_profile.argtypes = [_f32p] + [C.c_int] * 6 + [C.POINTER(C.c_double)] * 2
         L.ref_save_map.argtypes = [C.c_char_p, _f32p, C.c_int, C.c_int, C.c_int]
         L.ref_load_map.argtypes = [C.c_char_p, _f32p, C.c_int64] + [C.POINTER(C.c_int)] * 3
         L.ref_forward.argtypes = [_f32p] + [C.c_int] * 4 + [C.c_void_p] * 10 + [C.c_int, C.c_int,
@@ -318,6 +319,13 @@ class RefLib(_Lib):
 
     def hardware_concurrency(self):
         return self.lib.ref_hardware_concurrency()
+
+    def sparsity_profile(self, x, kw, kh, stride):
+        x = _f32(x)
+        raw, ext = C.c_double(), C.c_double()
+        self._chk(self.lib.ref_sparsity_profile(x.reshape(-1), *x.shape, kw, kh, stride,
+                                                C.byref(raw), C.byref(ext)))
+        return raw.value, ext.value
 
     def save_map(self, x, path):
         x = _f32(x)

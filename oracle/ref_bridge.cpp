@@ -313,6 +313,16 @@ int ref_forward(const float* x, int C, int H, int W, int nl, const int* k, const
   });
 }
 
+// sparsity_profile (dataset.cpp:270-286) of one map.
+int ref_sparsity_profile(const float* x, int C, int H, int W, int kw, int kh, int stride,
+                         double* raw, double* ext) {
+  return guarded([&] {
+    const auto p = sparsity_profile({as_map(x, C, H, W)}, kw, kh, stride);
+    *raw = p[0].raw;
+    *ext = p[0].extended;
+  });
+}
+
 // save / load (dataset.cpp:232-243) of the reference, FMAP or CSV by extension.
 int ref_save_map(const char* path, const float* x, int C, int H, int W) {
   return guarded([&] { save(as_map(x, C, H, W), path); });

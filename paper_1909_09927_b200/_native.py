@@ -26,7 +26,7 @@ SYMBOLS = (
     "sconv_cu_pecr_fill", "sconv_cu_pecr_pool", "sconv_shard", "sconv_cu_ecr_conv_multi",
     "sconv_cu_pecr_conv_pool_multi", "sconv_generate", "sconv_generate_batch", "sconv_checksum",
     "sconv_cu_forward", "sconv_cu_forward_dims", "sconv_io_last_error", "sconv_map_file_dims",
-    "sconv_load_map", "sconv_save_map", "sconv_load_maps",
+    "sconv_load_map", "sconv_save_map", "sconv_load_maps", "sconv_cu_window_nnz",
 )
 
 F_EXACT = 0
@@ -112,6 +112,7 @@ def lib() -> C.CDLL:
     L.sconv_cu_forward_dims.argtypes = [_vp, _i, _i, _i, _i] + [C.POINTER(_i)] * 3
     L.sconv_cu_forward.argtypes = [_vp, _vp] + [_i] * 4 + [_vp, _i, _i, _vp, _vp, _vp, _u64p,
                                                            _u64p, _vp, C.c_uint]
+    L.sconv_cu_window_nnz.argtypes = [_vp, _vp] + [_i] * 7 + [_vp, _vp, _vp, C.c_uint]
     L.sconv_io_last_error.restype = C.c_char_p
     L.sconv_map_file_dims.argtypes = [C.c_char_p] + [C.POINTER(_i)] * 3
     L.sconv_load_map.argtypes = [C.c_char_p, _vp, C.c_int64] + [C.POINTER(_i)] * 3

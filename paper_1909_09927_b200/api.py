@@ -844,6 +844,51 @@ def forward(net: NetworkSpec, input: FeatureMap, method: Method,
 # ---------------------------------------------------------------------------
 
 
+@dataclass
+class SparsityProfile:
+    """dataset.hpp:64-67."""
+    raw: float = 0.0
+    extended: float = 0.0  # zero fraction after im2col extension
+
+
+def window_nnz_counts(map: FeatureMap, k_w: int, k_h: int, stride: int,
+                      device: Optional[int] = None) -> List[int]:
+    """window_nnz_counts (dataset.cpp:249-268) on the GPU."""
+    od = conv_output_dims(map.width, map.height, k_w, k_h, stride)
+    out = np.empty(od.width * od.height, np.int32)
+    ctx = nat.context(0 if device is None else device)
+    ctx.use_own_stream()
+    v = np.ascontiguousarray(map.values, np.float32)
+    nat.check(nat.lib().sconv_cu_window_nnz(ctx.handle, _ptr(v), 1, map.channels, map.height,
+                                            map.width, k_h, k_w, stride, _ptr(out), None, None,
+                                            0), ctx.handle)
+    return out.tolist()
+
+
+def sparsity_profile(maps: Sequence[FeatureMap], k_w: int, k_h: int, stride: int,
+                     device: Optional[int] = None) -> List[SparsityProfile]:
+    """sparsity_profile (dataset.cpp:270-286) on the GPU: maps of equal dims
+    go in one batched call."""
+    ctx = nat.context(0 if device is None else device)
+    ctx.use_own_stream()
+    res = []
+    i = 0
+    while i < len(maps):
+        j = i
+        d = (maps[i].channels, maps[i].height, maps[i].width)
+        while j < len(maps) and (maps[j].channels, maps[j].height, maps[j].width) == d:
+            j += 1
+        x = np.stack([np.ascontiguousarray(m.values, np.float32) for m in maps[i:j]])
+        raw = np.empty(j - i, np.float64)
+        ext = np.empty(j - i, np.float64)
+        nat.check(nat.lib().sconv_cu_window_nnz(ctx.handle, _ptr(x), j - i, d[0], d[1], d[2], k_h,
+                                                k_w, stride, None, _ptr(raw), _ptr(ext), 0),
+                  ctx.handle)
+        res.extend(SparsityProfile(float(r), float(e)) for r, e in zip(raw, ext))
+        i = j
+    return res
+
+
 def _io_check(st: int) -> None:
     if st:
         from .errors import raise_for

@@ -301,6 +301,31 @@ __device__ __forceinline__ int window_nnz_at(const OpsArgs& a, const int32_t* pn
   return s;
 }
 
+// window_nnz_counts (src/dataset.cpp:249-268) for a batch: counts[n][oy][ox]
+// = nonzeros of window (oy, ox) over all channels, and per image the sum of
+// them and of the raw nonzeros (sparsity_profile, dataset.cpp:270-286).
+__global__ void window_nnz_kernel(const OpsArgs a, int32_t* __restrict__ counts,
+                                  unsigned long long* __restrict__ win_sum) {
+  const size_t per_img = static_cast<size_t>(a.OH) * a.OW;
+  const size_t total = static_cast<size_t>(a.N) * per_img;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t n = idx / per_img, r = idx % per_img;
+    const int nnz = window_nnz_at(a, a.pix + n * a.H * a.W, static_cast<int>(r / a.OW),
+                                  static_cast<int>(r % a.OW));
+    if (counts) counts[idx] = nnz;
+    if (win_sum && nnz) atomicAdd(win_sum + n, static_cast<unsigned long long>(nnz));  // integer: order-free
+  }
+}
+
+__global__ void pixel_sum_kernel(const int32_t* __restrict__ pix, int N, size_t plane,
+                                 unsigned long long* __restrict__ raw_sum) {
+  const size_t total = static_cast<size_t>(N) * plane;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x)
+    if (pix[idx]) atomicAdd(raw_sum + idx / plane, static_cast<unsigned long long>(pix[idx]));
+}
+
 __global__ void ops_kernel(const OpsArgs a) {
   unsigned long long muls = 0, adds = 0;
   const bool pecr = a.pw > 0;

@@ -948,6 +948,59 @@ int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int
   return SCONV_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Sparsity profiling (window_nnz_counts / sparsity_profile, src/dataset.cpp:249-286)
+// ---------------------------------------------------------------------------
+int sconv_cu_window_nnz(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, int kh,
+                        int kw, int stride, int32_t* counts, double* raw, double* extended,
+                        unsigned flags) {
+  if (!ctx) return fail(nullptr, SCONV_ERR_ARG, "null context");
+  if (n < 0) return fail(ctx, SCONV_ERR_SHAPE, "negative batch");
+  if (c < 1) return fail(ctx, SCONV_ERR_SHAPE, "channels must be positive");
+  int OW, OH;
+  TRY(conv_dims(ctx, w, h, kw, kh, stride, &OW, &OH));
+  if (n == 0) return SCONV_OK;
+  if (!x) return fail(ctx, SCONV_ERR_ARG, "null tensor pointer");
+  const bool dev = flags & SCONV_F_DEVICE;
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t x_elems = size_t(n) * c * h * w, plane = size_t(h) * w;
+  const size_t cnt_elems = size_t(n) * OH * OW;
+  Arena ar{ctx, {}};
+  const size_t i_x = dev ? 0 : ar.add(x_elems * 4);
+  const size_t i_pix = ar.add(size_t(n) * plane * 4);
+  const size_t i_cnt = (counts && !dev) ? ar.add(cnt_elems * 4) : 0;
+  const size_t i_sum = ar.add(size_t(n) * 16);
+  std::vector<char*> p;
+  TRY(ar.commit(p));
+  const float* dx = dev ? x : reinterpret_cast<float*>(p[i_x]);
+  if (!dev) CK(cudaMemcpyAsync(const_cast<float*>(dx), x, x_elems * 4, cudaMemcpyHostToDevice, st));
+  int32_t* pix = reinterpret_cast<int32_t*>(p[i_pix]);
+  int32_t* dcnt = counts ? (dev ? counts : reinterpret_cast<int32_t*>(p[i_cnt])) : nullptr;
+  auto* sums = reinterpret_cast<unsigned long long*>(p[i_sum]);  // [n] window, [n] raw
+  CK(cudaMemsetAsync(sums, 0, size_t(n) * 16, st));
+  pixel_nnz_kernel<<<grid_for(size_t(n) * plane, 256, ctx->num_sms), 256, 0, st>>>(dx, n, c, h, w, pix);
+  TRY(finish_launch(ctx, "pixel_nnz_kernel"));
+  OpsArgs oa{pix, n, h, w, kh, kw, stride, OH, OW, 0, 0, 0, 0, 0, nullptr};
+  window_nnz_kernel<<<grid_for(cnt_elems, 256, ctx->num_sms), 256, 0, st>>>(oa, dcnt, sums);
+  TRY(finish_launch(ctx, "window_nnz_kernel"));
+  pixel_sum_kernel<<<grid_for(size_t(n) * plane, 256, ctx->num_sms), 256, 0, st>>>(pix, n, plane,
+                                                                                 sums + n);
+  TRY(finish_launch(ctx, "pixel_sum_kernel"));
+  if (counts && !dev)
+    CK(cudaMemcpyAsync(counts, dcnt, cnt_elems * 4, cudaMemcpyDeviceToHost, st));
+  std::vector<unsigned long long> h_sums(size_t(n) * 2);
+  CK(cudaMemcpyAsync(h_sums.data(), sums, size_t(n) * 16, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // sparsity(): zero fraction of the map; extended: zero fraction of im2col
+  const double map_sz = double(c) * h * w, col_sz = double(OH) * OW * c * kh * kw;
+  for (int i = 0; i < n; ++i) {
+    if (raw) raw[i] = double(uint64_t(map_sz) - h_sums[n + i]) / map_sz;
+    if (extended) extended[i] = double(uint64_t(col_sz) - h_sums[i]) / col_sz;
+  }
+  return SCONV_OK;
+}
+
 int sconv_cu_ecr_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w,
                       const float* filters, int k, int kh, int kw, int stride, float* y,
                       uint64_t* muls, uint64_t* adds, unsigned flags) {

@@ -592,3 +592,24 @@ def test_async_host_calls(sc, orc):
         sc.synchronize()
         for o, r in zip(outs, want):
             assert bits_equal(o, r)
+
+
+def test_sparsity_profiling(sc, orc, ref):
+    """window_nnz_counts / sparsity_profile (dataset.cpp:249-286) on the GPU:
+    integer window counts equal the oracle's, ratios equal the reference's."""
+    maps = []
+    for i, (c, h, w, s) in enumerate([(3, 20, 17, 0.7), (3, 20, 17, 0.95), (8, 9, 9, 0.0),
+                                      (1, 6, 6, 1.0)]):
+        m = orc.generate(h, w, c, s, 70 + i)
+        maps.append(sc.FeatureMap(c, h, w, m.reshape(-1)))
+    for kk, stride in ((3, 1), (2, 2), (5, 3)):
+        for m in maps:
+            if kk > min(m.height, m.width):
+                continue
+            got = sc.window_nnz_counts(m, kk, kk, stride)
+            want = orc.window_nnz(m.array(), kk, kk, stride).reshape(-1).tolist()
+            assert got == want
+        prof = sc.sparsity_profile([m for m in maps if kk <= min(m.height, m.width)], kk, kk,
+                                   stride)
+        for p, m in zip(prof, [m for m in maps if kk <= min(m.height, m.width)]):
+            assert (p.raw, p.extended) == ref.sparsity_profile(m.array(), kk, kk, stride)
