@@ -82,6 +82,13 @@ __device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool v
                : "memory");
 }
 
+// 8-byte copy, src_bytes in {0, 4, 8}: the rest of the 8 bytes is zero-filled.
+__device__ __forceinline__ void cp_async8(float* smem, const float* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(float* smem, const float* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   const int bytes = valid ? 16 : 0;

@@ -54,6 +54,12 @@ struct WsCfg {
   static constexpr int SMEM_BYTES = NS * STAGE * 4 + 2 * NS * 8;
   static constexpr int CELLS = WPC * NPOS;           // input cells per channel
   static constexpr int CELLS_PER_LANE = (CELLS + 31) / 32;
+  // Producer copies cells in 8-byte pairs when every window row starts on an
+  // even column (even row width, even tile stride and map width): half the
+  // cp.async instructions and requests.
+  static constexpr bool PAIR = (WPW % 2 == 0) && ((TW * S) % 2 == 0);
+  static constexpr int PAIRS = WPC * NPOS / 2;
+  static constexpr int PAIRS_PER_LANE = (PAIRS + 31) / 32;
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
   static_assert(R == 2 || R == 4 || R == 8, "R");
   static_assert(P == 0 || (TH % P == 0 && TW % P == 0), "pool tile");
@@ -195,6 +201,54 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
   if (warp == WPC) {
     // ------------------------------ producer ------------------------------
     const size_t plane = static_cast<size_t>(H) * W;
+    if constexpr (Cfg::PAIR) {
+      if ((W & 1) == 0) {  // warp-uniform: 8-byte aligned cell pairs
+        int src_off[Cfg::PAIRS_PER_LANE];
+        int dst_off[Cfg::PAIRS_PER_LANE];
+        int bytes[Cfg::PAIRS_PER_LANE];
+#pragma unroll
+        for (int e = 0; e < Cfg::PAIRS_PER_LANE; ++e) {
+          const int q = lane + 32 * e;
+          const int wi = q / (Cfg::NPOS / 2), pp = q - wi * (Cfg::NPOS / 2);
+          const int Y = pp / (WPW / 2), X = 2 * (pp - Y * (WPW / 2));
+          const int t = cta * WPC + wi;
+          const int n = t / a.tiles_per_img, tt = t - n * a.tiles_per_img;
+          const int ty = tt / a.tiles_x, tx = tt - ty * a.tiles_x;
+          const int iy = ty * TH * S + Y, ix = tx * TW * S + X;
+          const bool ok = q < Cfg::PAIRS && t < a.total_tiles && iy < H && ix < W;
+          bytes[e] = ok ? (ix + 1 < W ? 8 : 4) : 0;
+          src_off[e] = ok ? static_cast<int>((static_cast<size_t>(n) * C * H + iy) * W + ix) : 0;
+          dst_off[e] = (wi * CC) * PATCH + Y * PITCH + X;
+        }
+        if (lane == 0)
+          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
+        for (int k = 0; k < nchunks; ++k) {
+          const int s = k % NS;
+          if (k >= NS) mbar_wait_sleep(&empty[s], ((k / NS) + 1) & 1);
+          float* in_s = smem + s * Cfg::STAGE;
+          float* w_s = in_s + Cfg::IN_STAGE;
+          const int c0 = k * CC;
+#pragma unroll
+          for (int e = 0; e < Cfg::PAIRS_PER_LANE; ++e) {
+            if (lane + 32 * e < Cfg::PAIRS) {
+#pragma unroll
+              for (int ch = 0; ch < CC; ++ch) {
+                const int b = c0 + ch < C ? bytes[e] : 0;
+                const float* src = b ? a.x + src_off[e] + (c0 + ch) * plane : a.x;
+                cp_async8(in_s + dst_off[e] + ch * PATCH, src, b);
+              }
+            }
+          }
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&full[s], Cfg::W_BYTES);
+            tma_load_3d(w_s, &wmap, k0, 0, c0, &full[s]);
+          }
+          mbar_arrive_cp_async(&full[s]);
+        }
+        cp_async_wait<0>();
+        return;
+      }
+    }
     int src_off[Cfg::CELLS_PER_LANE];
     int dst_off[Cfg::CELLS_PER_LANE];
     bool ok[Cfg::CELLS_PER_LANE];
