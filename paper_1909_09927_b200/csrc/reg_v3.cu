@@ -35,11 +35,12 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P) {
     if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
     return 1;
   }
-  // Measured on B200 (tools/tune.py, profiles/r01): with the filters staged
-  // by TMA, v3 beats v2 on every K >= 128 VGG layer (17-20%); for K = 64 the
-  // 6x6-tile WsG wins at sparsity 0.7 (5%) once there are enough channel
-  // chunks to fill the producer pipeline (conv1_1's C = 3 stays on v2).
-  if (K < 128) return C >= 16 ? 7 : 0;
+  // Measured on B200 (tools/tune.py, tools/ksweep.py, profiles/r01): with the
+  // filters staged by TMA, v3 beats v2 on every K >= 128 VGG layer (17-20%);
+  // for K = 64 PECR the 6x6-tile WsG wins (its pooled 3x3 stores are small),
+  // for K = 64 ECR the 4x4-tile WsD (float4 stores, 3 CTAs/SM: conv1_2 3588
+  // -> 3320 us); small C goes to the small-C kernel before this is asked.
+  if (K < 128) return C >= 16 ? (P == 2 ? 7 : 4) : 0;
   if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
   return 1;
 }
