@@ -58,6 +58,13 @@ struct WsCfg {
   // even column (even row width, even tile stride and map width): half the
   // cp.async instructions and requests.
   static constexpr bool PAIR = (WPW % 2 == 0) && ((TW * S) % 2 == 0);
+  // Channels whose window density is at most SPARSE_PCT percent take the
+  // row-skipping, fully branched body; denser ones the body whose 1-3-tap
+  // border cells ptxas predicates (their FFMA2 run even for zero cells).
+  // Measured (A/B, tools/gpu_ab2.sh): with R = 2 or 2-row tiles the border
+  // cells carry so little work that branching always wins (conv5 2x7 -3.5%,
+  // conv1_2 ECR -2.3%); 4x4 R = 4 tiles prefer predication above 25%.
+  static constexpr int SPARSE_PCT = (R <= 2 || TH <= 2) ? 100 : 25;
   static constexpr int PAIRS = WPC * NPOS / 2;
   static constexpr int PAIRS_PER_LANE = (PAIRS + 31) / 32;
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
@@ -330,7 +337,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
 #pragma unroll
         for (int ij = 0; ij < KK; ++ij) ws_lds_w<R>(wr[ij], wsrc + ij * KT, lane);
 
-        if ((__popc(m0) + __popc(m1)) * 4 <= Cfg::NPOS)
+        if ((__popc(m0) + __popc(m1)) * 100 <= Cfg::NPOS * Cfg::SPARSE_PCT)
           ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, true>(acc, wr, ic, m0, m1);
         else
           ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, false>(acc, wr, ic, m0,
