@@ -34,6 +34,10 @@
 
 namespace sconv_cu {
 
+#ifndef SCONV_SPARSE_PCT_WIDE  // see WsCfg::SPARSE_PCT
+#define SCONV_SPARSE_PCT_WIDE 25
+#endif
+
 template <int KH_, int KW_, int S_, int TH_, int TW_, int R_, int WPC_, int CC_, int NS_, int P_>
 struct WsCfg {
   static constexpr int KH = KH_, KW = KW_, S = S_, TH = TH_, TW = TW_, R = R_;
@@ -64,7 +68,7 @@ struct WsCfg {
   // Measured (A/B, tools/gpu_ab2.sh): with R = 2 or 2-row tiles the border
   // cells carry so little work that branching always wins (conv5 2x7 -3.5%,
   // conv1_2 ECR -2.3%); 4x4 R = 4 tiles prefer predication above 25%.
-  static constexpr int SPARSE_PCT = (R <= 2 || TH <= 2) ? 100 : 25;
+  static constexpr int SPARSE_PCT = (R <= 2 || TH <= 2) ? 100 : SCONV_SPARSE_PCT_WIDE;
   static constexpr int PAIRS = WPC * NPOS / 2;
   static constexpr int PAIRS_PER_LANE = (PAIRS + 31) / 32;
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
