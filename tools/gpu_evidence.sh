@@ -7,7 +7,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 tail -2 gpurun_out/pytest_gpu.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-   python bench.py --steps 1 --warmup 0 --no-cudnn --no-e2e --no-cpu --no-forward > gpurun_out/bench_ncu.log 2>&1
+   python bench.py --steps 1 --warmup 0 --no-cudnn --no-e2e --no-cpu --no-forward --no-check > gpurun_out/bench_ncu.log 2>&1
 LAYER=512,512,28 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ecr_ -s 2 -c 1 \
    -o gpurun_out/prof_conv4_2 python tools/ncu_one.py > gpurun_out/ncu_full.log 2>&1
 LAYER=64,64,224 POOL=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ecr_ -s 2 -c 1 \
