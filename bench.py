@@ -382,18 +382,22 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         per = []
-        for l in range(nl):
-            e0.record(stream)
+        for l in range(nl):  # best of 3 trials of 3 launches: cuDNN at its fastest
+            best = None
             for _ in range(3):
-                dense(l)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            per.append(e0.elapsed_time(e1) / 3)
+                e0.record(stream)
+                for _ in range(3):
+                    dense(l)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) / 3
+                best = t if best is None else min(best, t)
+            per.append(best)
         cudnn = {"ms_per_step": sum(per), "us_per_layer": sum(per) * 1e3 / nl,
                  "layers_us": {VGG19[l][0]: per[l] * 1e3 for l in range(nl)},
                  "speedup_ours_vs_cudnn": sum(per) / ms_per_step,
                  "settings": "torch conv2d(padding=0)+relu+max_pool2d, fp32, TF32 off, "
-                             "cudnn.benchmark=True"}
+                             "cudnn.benchmark=True, best of 3 trials per layer"}
 
     # ---- e2e through the C ABI with pinned host buffers --------------------
     e2e = None
