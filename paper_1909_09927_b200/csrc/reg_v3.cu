@@ -42,7 +42,12 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P) {
   // -> 3320 us); small C goes to the small-C kernel before this is asked.
   if (K < 128) return C >= 16 ? (P == 2 ? 7 : 4) : 0;
   if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
-  return 1;
+  // One CTA of 15 consumer warps per SM (WsA) beats two CTAs of 7 (WsE) once
+  // there are enough channel chunks to amortise a CTA's pipeline fill and
+  // drain (C >= 128): one producer per SM instead of two, and finer last
+  // waves (conv4_2 2638 -> 2451 us, conv4_1 -6%, conv3_2 / conv2_2 -2%);
+  // with C = 64 (16 chunks) the overlap of two CTAs wins (conv2_1 1302 vs 1366).
+  return C >= 128 ? 1 : 5;
 }
 
 // Plan of a v3 launch: kernel id 100 + registry index; grid_x counts CTAs of

@@ -115,11 +115,14 @@ def test_launch_plan(sc):
     # K = 64: v3 with 6x6 tiles (WsG)
     p = sc.launch_plan(64, 64, 226, 226, 64, 3, 3, 1, sc.PoolConfig(2, 2, 2))
     assert p["kernel"] == 107 and p["smem_bytes"] <= 227 * 1024
-    # K >= 128: v3 warp-specialised kernel, 7 consumer warps (4x4 tiles) + 1 producer
+    # K >= 128, C >= 128: v3 warp-specialised kernel, 15 consumer warps (4x4 tiles) + 1
+    # producer, one CTA per SM; linear grid, K-blocks fastest: ceil(tiles / 15) x 4
     p = sc.launch_plan(64, 512, 30, 30, 512, 3, 3, 1)
-    # linear grid, K-blocks fastest: (tiles / 7 CTAs) x 4 K-blocks
-    assert p["kernel"] == 101 and p["grid_y"] == 1 and p["block_threads"] == 256
-    assert p["grid_x"] == 64 * 7 * 7 // 7 * 4 and p["grid_z"] == 1
+    assert p["kernel"] == 101 and p["grid_y"] == 1 and p["block_threads"] == 512
+    assert p["grid_x"] == (64 * 7 * 7 + 14) // 15 * 4 and p["grid_z"] == 1
+    # C < 128: two CTAs of 7 consumers per SM (WsE)
+    p = sc.launch_plan(64, 64, 114, 114, 128, 3, 3, 1)
+    assert p["kernel"] == 105 and p["block_threads"] == 256
     p = sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1)  # 14x14 maps: 2x7 tiles, no waste
     assert p["kernel"] == 102 and p["grid_x"] == 64 * 2 * 4 and p["grid_y"] == 1
     # 5x5 / 1x1 windows: the v3 kernel instantiated for them; other shapes: generic
