@@ -16,7 +16,7 @@ bool ws_applies(int id, int K, int kh, int kw, int S, int P) {
   return false;
 }
 
-int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P) {
+int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4) {
   if (!((P == 0 || P == 2) && K >= 32)) return 0;
   // strided 3x3 (the paper's stride-2/3 experiments):
   // 2x2 output tiles whose 5x5 / 6x6 input windows fit the 64-bit mask
@@ -46,8 +46,10 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P) {
   // there are enough channel chunks to amortise a CTA's pipeline fill and
   // drain (C >= 128): one producer per SM instead of two, and finer last
   // waves (conv4_2 2638 -> 2451 us, conv4_1 -6%, conv3_2 / conv2_2 -2%);
-  // with C = 64 (16 chunks) the overlap of two CTAs wins (conv2_1 1302 vs 1366).
-  return C >= 128 ? 1 : 5;
+  // with C = 64 (16 chunks) the overlap of two CTAs wins (conv2_1 1302 vs 1366),
+  // and so it does for grids of fewer than ~2 waves of the big CTAs (batch-1
+  // forward: 4.0 vs 5.2 ms).  tiles4 = 4x4 output tiles x K-blocks of 128.
+  return (C >= 128 && tiles4 >= 2L * 148 * 15) ? 1 : 5;
 }
 
 // Plan of a v3 launch: kernel id 100 + registry index; grid_x counts CTAs of
