@@ -420,12 +420,12 @@ def main():
                     sc.ecr_conv_batched(xs[l], ws[l], 1, fast=fast, out=ys[l], device=local,
                                         sync=False)
             sc.synchronize(local)
-        for _ in range(2):  # sizes the per-call workspaces and the memory pool
+        for _ in range(3):  # sizes the per-call workspaces and the memory pool
             e2e_step()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        e2e_steps = max(1, min(args.steps, 3))
+        e2e_steps = max(1, min(args.steps, 5))
         for _ in range(e2e_steps):
             e2e_step()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps

@@ -123,8 +123,10 @@ def test_launch_plan(sc):
     # C < 128: two CTAs of 7 consumers per SM (WsE)
     p = sc.launch_plan(64, 64, 114, 114, 128, 3, 3, 1)
     assert p["kernel"] == 105 and p["block_threads"] == 256
-    p = sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1)  # 14x14 maps: 2x7 tiles, no waste
-    assert p["kernel"] == 102 and p["grid_x"] == 64 * 2 * 4 and p["grid_y"] == 1
+    p = sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1)  # 14x14 maps, big grid: 15-warp CTAs
+    assert p["kernel"] == 101
+    p = sc.launch_plan(8, 512, 16, 16, 512, 3, 3, 1)  # small grid: waste-free 2x7 tiles
+    assert p["kernel"] == 102 and p["grid_x"] == 8 * 2 * 4 and p["grid_y"] == 1
     # 5x5 / 1x1 windows: the v3 kernel instantiated for them; other shapes: generic
     assert sc.launch_plan(1, 20, 11, 11, 50, 5, 5, 1)["kernel"] == 110
     assert sc.launch_plan(1, 480, 14, 14, 192, 1, 1, 1)["kernel"] == 108
