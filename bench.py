@@ -424,10 +424,13 @@ def main():
             e2e_step()
         if world > 1:
             dist.barrier()
-        t0 = time.perf_counter()
         e2e_steps = max(1, min(args.steps, 5))
+        e2e_each = []
+        t0 = time.perf_counter()
         for _ in range(e2e_steps):
+            t1 = time.perf_counter()
             e2e_step()
+            e2e_each.append(round((time.perf_counter() - t1) * 1e3, 2))
         e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
         if world > 1:
             t = torch.tensor([e2e_ms], device=dev)
@@ -436,7 +439,7 @@ def main():
         h2d = sum(in_bytes) + sum(w_bytes)
         d2h = sum(out_bytes)
         e2e = {"value": e2e_ms * 1e3 / nl / world, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "ms_each_step": e2e_each,
                "path": "sconv_cu_ecr_conv / sconv_cu_pecr_conv_pool with pinned host pointers, "
                        "SCONV_F_ASYNC per layer + one sconv_cu_synchronize per step"}
 
