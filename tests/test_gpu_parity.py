@@ -613,3 +613,32 @@ def test_sparsity_profiling(sc, orc, ref):
                                    stride)
         for p, m in zip(prof, [m for m in maps if kk <= min(m.height, m.width)]):
             assert (p.raw, p.extended) == ref.sparsity_profile(m.array(), kk, kk, stride)
+
+
+@pytest.mark.parametrize("kid", [0, 1, "A", "D", "E", "G", "M", "generic"])
+def test_signed_zeros_and_negative_inputs(sc, orc, kid):
+    """-0.0 is a zero (`v != 0.0f`, src/ecr.cpp:79-93 / src/pecr.cpp:114-125)
+    and negative values are nonzeros: every kernel family must skip the
+    former, keep the latter, and give the oracle's bits and counters."""
+    c, k = (3, 64) if kid == "M" else (13, 128 if kid in ("A", "E") else 64)
+    x, f = inputs(orc, 2, c, 18, 18, k, 3, 3, 0.6, seed=515)
+    rng = np.random.default_rng(5)
+    zeros = x == 0
+    x[zeros & (rng.random(x.shape) < 0.5)] = np.float32(-0.0)
+    x[~zeros & (rng.random(x.shape) < 0.3)] *= np.float32(-1.0)
+    assert np.signbit(x[zeros]).any() and (x < 0).any()
+    generic = kid == "generic"
+    kernel = 0 if generic else kid
+    ref, rops = orc.ecr_conv(x, f, 1)
+    ops = sc.OpCount()
+    y = sc.ecr_conv_batched(x, f, 1, counters=ops, generic=generic, kernel=kernel)
+    assert bits_equal(y, ref) and (ops.multiplications, ops.additions) == rops
+    assert close(sc.ecr_conv_batched(x, f, 1, fast=True, generic=generic, kernel=kernel), ref)
+    # the same map with +0.0 everywhere gives the same bits
+    xp = np.where(zeros, np.float32(0.0), x).astype(np.float32)
+    assert bits_equal(sc.ecr_conv_batched(xp, f, 1, generic=generic, kernel=kernel), y)
+    pool = sc.PoolConfig(2, 2, 2)
+    pref, pops = orc.pecr_conv(x, f, 1, 2, 2, 2, 0)
+    ops = sc.OpCount()
+    p = sc.pecr_conv_pool_batched(x, f, 1, pool, counters=ops, generic=generic, kernel=kernel)
+    assert bits_equal(p, pref) and (ops.multiplications, ops.additions) == pops
