@@ -72,7 +72,8 @@ int launch_tiled(sconv_cu_ctx* ctx, bool fast, int which, int P, const TiledArgs
 void plan_for(sconv_launch_plan* p, int which, int N, int K, int OH, int OW);
 
 // v3 warp-specialised registry (reg_v3.cu / reg_v3_exact.cu / reg_v3_fast.cu).
-int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4 = 1L << 40);
+int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4 = 1L << 40,
+            long tiles2 = 1L << 40);
 bool ws_applies(int id, int K, int kh, int kw, int S, int P);  // forced-config shape check
 int launch_ws_fast(sconv_cu_ctx* ctx, int which, int P, const WsArgs& a);
 int launch_ws_exact(sconv_cu_ctx* ctx, int which, int P, const WsArgs& a);

@@ -11,12 +11,13 @@ bool ws_applies(int id, int K, int kh, int kw, int S, int P) {
   if (id == 12) return kh == 3 && kw == 3 && S == 3;
   if (S != 1) return false;
   if (id >= 1 && id <= 7) return kh == 3 && kw == 3 && !(id == 2 && P != 0);
-  if (id == 8 || id == 9) return kh == 1 && kw == 1;
-  if (id == 10) return kh == 5 && kw == 5;
+  if (id == 8 || id == 9 || id == 14 || id == 15) return kh == 1 && kw == 1;
+  if (id == 10 || id == 17) return kh == 5 && kw == 5;
+  if (id == 16) return kh == 3 && kw == 3;
   return false;
 }
 
-int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4) {
+int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4, long tiles2) {
   if (!((P == 0 || P == 2) && K >= 32)) return 0;
   // strided 3x3 (the paper's stride-2/3 experiments):
   // 2x2 output tiles whose 5x5 / 6x6 input windows fit the 64-bit mask
@@ -24,8 +25,20 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4) {
   if (S != 1) return 0;
   // 1x1 / 5x5 (GoogLeNet / LeNet layers, BASELINE config 2): the same
   // warp-specialised kernel instantiated for that window (tools/config2.py)
-  if (kh == 1 && kw == 1) return K >= 128 ? 8 : 9;
-  if (kh == 5 && kw == 5) return 10;
+  //
+  // Maps too small to fill the GPU with 4x4 tiles take 2x2 tiles (WsN-WsQ)
+  // when those still fit in one wave of 7-consumer CTAs at 2 per SM: on every
+  // config-2 layer (tools/config2.py, profiles/r01/config2_layers.jsonl) this
+  // picks the faster of the two (AlexNet conv3 114 -> 71 us, inception 5a 1x1
+  // 138 -> 101 us, 5b 5x5 34 -> 26 us; 4a's 12x12 3x3 stays on 4x4 tiles:
+  // 62 vs 104 us).  tiles2 = images x 2x2 output tiles.
+  const long wave = 148L * 2 * 7;
+  const long kb128 = (K + 127) / 128, kb64 = (K + 63) / 64;
+  if (kh == 1 && kw == 1) {
+    if (K >= 128) return tiles2 * kb128 <= wave ? 14 : 8;
+    return tiles2 * kb64 <= wave ? 15 : 9;
+  }
+  if (kh == 5 && kw == 5) return tiles2 * kb64 <= wave ? 17 : 10;
   if (!(kh == 3 && kw == 3)) return 0;
   const char* e = std::getenv("SCONV_KERNEL");
   if (e && std::strcmp(e, "v2") == 0) return 0;
@@ -40,6 +53,7 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4) {
   // for K = 64 PECR the 6x6-tile WsG wins (its pooled 3x3 stores are small),
   // for K = 64 ECR the 4x4-tile WsD (float4 stores, 3 CTAs/SM: conv1_2 3588
   // -> 3320 us); small C goes to the small-C kernel before this is asked.
+  if (K >= 128 && tiles2 * kb128 <= wave) return 16;
   if (K < 128) return C >= 16 ? (P == 2 ? 7 : 4) : 0;
   // (with the 15-consumer CTA the 4x4 tiles beat the waste-free 2x7 tiles on
   // 14x14 maps too: conv5_1 819 -> 797 us)
@@ -87,6 +101,10 @@ void plan_ws(sconv_launch_plan* out, int ws, int n, int k, int OH, int OW) {
     case 10: plan_ws_t<WsJ<0>>(out, ws, n, k, OH, OW); break;
     case 11: plan_ws_t<WsK<0>>(out, ws, n, k, OH, OW); break;
     case 12: plan_ws_t<WsL<0>>(out, ws, n, k, OH, OW); break;
+    case 14: plan_ws_t<WsN<0>>(out, ws, n, k, OH, OW); break;
+    case 15: plan_ws_t<WsO<0>>(out, ws, n, k, OH, OW); break;
+    case 16: plan_ws_t<WsP<0>>(out, ws, n, k, OH, OW); break;
+    case 17: plan_ws_t<WsQ<0>>(out, ws, n, k, OH, OW); break;
     default: plan_ws_t<WsC<0>>(out, ws, n, k, OH, OW); break;
   }
 }

@@ -178,11 +178,12 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   const int Pk = pecr ? (P ? P : -1) : 0;
   const int forced = (flags >> 8) & 0xff;
   const long tiles4 = long(n) * ((OH + 3) / 4) * ((OW + 3) / 4) * ((k + 127) / 128);
+  const long tiles2 = long(n) * ((OH + 1) / 2) * ((OW + 1) / 2);
   // few input channels (VGG conv1_1): the per-warp small-C kernel (smallc.cuh)
   const bool smallc_ok = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
   bool smallc = !(flags & SCONV_F_GENERIC) && smallc_ok &&
                 (((flags >> 8) & 0xff) == 'M' || (!((flags >> 8) & 0xff) && c <= 4));
-  int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk, tiles4);
+  int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk, tiles4, tiles2);
   int which = (flags & SCONV_F_GENERIC) || ws || smallc ? 0 : pick_tiled(k, kh, kw, stride, Pk);
   // PECR with a pool the fused epilogue does not cover (anything but 2x2/2):
   // a tiled kernel computes the conv into a workspace, then
@@ -191,7 +192,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   if (pecr && Pk != 2 && !ws && !which && !smallc && !(flags & SCONV_F_GENERIC) &&
       !((flags >> 8) & 0xff)) {
     smallc = kh == 3 && kw == 3 && stride == 1 && k >= 32 && c <= 4;
-    ws = smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0, tiles4);
+    ws = smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0, tiles4, tiles2);
     which = smallc || ws ? 0 : pick_tiled(k, kh, kw, stride, 0);
     pool_after = smallc || ws || which;
   }
@@ -204,7 +205,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
         which = forced;
         ws = 0;
       }
-    } else if (forced >= 'A' && forced <= 'L') {
+    } else if (forced >= 'A' && forced <= 'Q') {
       if (ws_applies(forced - 'A' + 1, k, kh, kw, stride, Pk)) {
         ws = forced - 'A' + 1;
         which = 0;
@@ -674,14 +675,15 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
   }
   const int forced = (flags >> 8) & 0xff;
   const long tiles4 = long(n) * ((OH + 3) / 4) * ((OW + 3) / 4) * ((k + 127) / 128);
+  const long tiles2 = long(n) * ((OH + 1) / 2) * ((OW + 1) / 2);
   bool smallc = !(flags & SCONV_F_GENERIC) && kh == 3 && kw == 3 && stride == 1 &&
                 (P == 0 || P == 2) && k >= 32 && (forced == 'M' || (!forced && c <= 4));
-  int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, P, tiles4);
+  int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, P, tiles4, tiles2);
   int which = (flags & SCONV_F_GENERIC) || ws || smallc ? 0 : pick_tiled(k, kh, kw, stride, P);
   if (pool_w > 0 && P != 2 && !ws && !which && !smallc && !(flags & SCONV_F_GENERIC) && !forced) {
     // conv by a tiled kernel, then pecr_pool_fold_kernel (see fused_conv)
     smallc = kh == 3 && kw == 3 && stride == 1 && k >= 32 && c <= 4;
-    ws = smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0, tiles4);
+    ws = smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0, tiles4, tiles2);
     which = smallc || ws ? 0 : pick_tiled(k, kh, kw, stride, 0);
   }
   if (smallc) {

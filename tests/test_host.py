@@ -125,11 +125,19 @@ def test_launch_plan(sc):
     assert p["kernel"] == 105 and p["block_threads"] == 256
     p = sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1)  # 14x14 maps, big grid: 15-warp CTAs
     assert p["kernel"] == 101
-    p = sc.launch_plan(8, 512, 16, 16, 512, 3, 3, 1)  # small grid: waste-free 2x7 tiles
-    assert p["kernel"] == 102 and p["grid_x"] == 8 * 2 * 4 and p["grid_y"] == 1
+    p = sc.launch_plan(16, 512, 16, 16, 512, 3, 3, 1)  # under a wave: waste-free 2x7 tiles
+    assert p["kernel"] == 102 and p["grid_x"] == 16 * 2 * 4 and p["grid_y"] == 1
+    # 2x2 tiles fit in one wave of 7-consumer CTAs (148 x 2 x 7 warp tiles): 2x2 tiles
+    p = sc.launch_plan(8, 512, 16, 16, 512, 3, 3, 1)
+    assert p["kernel"] == 116 and p["grid_x"] == 8 * 49 // 7 * 4 and p["tile_h"] == 2
+    assert sc.launch_plan(1, 512, 30, 30, 512, 3, 3, 1)["kernel"] == 116
+    assert sc.launch_plan(1, 64, 114, 114, 128, 3, 3, 1)["kernel"] == 105
     # 5x5 / 1x1 windows: the v3 kernel instantiated for them; other shapes: generic
-    assert sc.launch_plan(1, 20, 11, 11, 50, 5, 5, 1)["kernel"] == 110
-    assert sc.launch_plan(1, 480, 14, 14, 192, 1, 1, 1)["kernel"] == 108
+    assert sc.launch_plan(64, 32, 18, 18, 128, 5, 5, 1)["kernel"] == 110
+    assert sc.launch_plan(64, 48, 7, 7, 128, 5, 5, 1)["kernel"] == 117
+    assert sc.launch_plan(64, 480, 14, 14, 192, 1, 1, 1)["kernel"] == 108
+    assert sc.launch_plan(64, 832, 7, 7, 256, 1, 1, 1)["kernel"] == 114
+    assert sc.launch_plan(64, 480, 7, 7, 64, 1, 1, 1)["kernel"] == 115
     assert sc.launch_plan(1, 3, 227, 227, 96, 11, 11, 4)["kernel"] == 0
 
 

@@ -65,10 +65,18 @@ def main():
             return e0.elapsed_time(e1) / reps * 1e3
         ours = tm(lambda: sc.ecr_conv_batched(xt, wt, 1, fast=True, sync=False))
         cud = tm(lambda: torch.nn.functional.conv2d(xt, wt))
-        print(json.dumps({"layer": name, "C": C, "K": K, "k": k, "size": size, "sparsity": s,
-                          "N": N, "kernel": plan["kernel"], "exact_bitwise_vs_oracle": exact,
-                          "ours_us": round(ours, 2), "cudnn_us": round(cud, 2),
-                          "speedup_vs_cudnn": round(cud / ours, 3)}), flush=True)
+        row = {"layer": name, "C": C, "K": K, "k": k, "size": size, "sparsity": s,
+               "N": N, "kernel": plan["kernel"], "exact_bitwise_vs_oracle": exact,
+               "ours_us": round(ours, 2), "cudnn_us": round(cud, 2),
+               "speedup_vs_cudnn": round(cud / ours, 3)}
+        # KIDS=A,E,N,...: also time forced configs (dev sweep)
+        for kid in filter(None, os.environ.get("KIDS", "").split(",")):
+            try:
+                row["us_" + kid] = round(tm(lambda: sc.ecr_conv_batched(
+                    xt, wt, 1, fast=True, sync=False, kernel=kid)), 2)
+            except Exception as e:  # config does not apply to this window
+                row["us_" + kid] = str(e)[:24]
+        print(json.dumps(row), flush=True)
 
 
 if __name__ == "__main__":
