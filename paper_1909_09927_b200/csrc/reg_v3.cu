@@ -55,18 +55,19 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4, lon
   // -> 3320 us); small C goes to the small-C kernel before this is asked.
   if (K >= 128 && tiles2 * kb128 <= wave) return 16;
   if (K < 128) return C >= 16 ? (P == 2 ? 7 : 4) : 0;
-  // (with the 15-consumer CTA the 4x4 tiles beat the waste-free 2x7 tiles on
-  // 14x14 maps too: conv5_1 819 -> 797 us)
-  if (C >= 128 && tiles4 >= 148L * 15) return 1;
-  if (OW % 4 != 0 && OW % 7 == 0 && P == 0) return 2;
   // One CTA of 15 consumer warps per SM (WsA) beats two CTAs of 7 (WsE) once
   // there are enough channel chunks to amortise a CTA's pipeline fill and
   // drain (C >= 128): one producer per SM instead of two, and finer last
   // waves (conv4_2 2638 -> 2451 us, conv4_1 -6%, conv3_2 / conv2_2 -2%);
-  // with C = 64 (16 chunks) the overlap of two CTAs wins (conv2_1 1302 vs 1366),
-  // and so it does for grids of less than one wave of the big CTAs (batch-1
-  // forward: 4.0 vs 5.2 ms).  tiles4 = 4x4 output tiles x K-blocks of 128.
-  return (C >= 128 && tiles4 >= 148L * 15) ? 1 : 5;
+  // with C = 64 (16 chunks) the overlap of two CTAs wins (conv2_1 1302 vs
+  // 1366).  Below one wave WsA leaves SMs idle that WsE's smaller CTAs still
+  // reach; tools/smallgrid.py over batches 2-32 of the C >= 128 VGG layers
+  // puts the crossover between 1024 (WsE 311 vs 414 us) and 1568 (WsA 418 vs
+  // 450 us) warp tiles.  With the 15-consumer CTA the 4x4 tiles also beat the
+  // waste-free 2x7 tiles (WsB) on 14x14 maps at every batch measured (conv5_1
+  // at 64: 797 vs 819 us; at 16: WsE 311 vs WsB 319 us), so WsB is forced-only.
+  // tiles4 = 4x4 output tiles x K-blocks of 128.
+  return (C >= 128 && tiles4 >= 148L * 10) ? 1 : 5;
 }
 
 // Plan of a v3 launch: kernel id 100 + registry index; grid_x counts CTAs of

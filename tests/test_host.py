@@ -125,8 +125,11 @@ def test_launch_plan(sc):
     assert p["kernel"] == 105 and p["block_threads"] == 256
     p = sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1)  # 14x14 maps, big grid: 15-warp CTAs
     assert p["kernel"] == 101
-    p = sc.launch_plan(16, 512, 16, 16, 512, 3, 3, 1)  # under a wave: waste-free 2x7 tiles
-    assert p["kernel"] == 102 and p["grid_x"] == 16 * 2 * 4 and p["grid_y"] == 1
+    # under ~2/3 of a wave of 15-warp CTAs: two 7-warp CTAs per SM (WsE)
+    p = sc.launch_plan(16, 512, 16, 16, 512, 3, 3, 1)
+    assert p["kernel"] == 105 and p["grid_x"] == (16 * 16 + 6) // 7 * 4 and p["grid_y"] == 1
+    assert sc.launch_plan(8, 512, 30, 30, 512, 3, 3, 1)["kernel"] == 101  # 1568 warp tiles
+    assert sc.launch_plan(4, 512, 30, 30, 512, 3, 3, 1)["kernel"] == 105  # 784
     # 2x2 tiles fit in one wave of 7-consumer CTAs (148 x 2 x 7 warp tiles): 2x2 tiles
     p = sc.launch_plan(8, 512, 16, 16, 512, 3, 3, 1)
     assert p["kernel"] == 116 and p["grid_x"] == 8 * 49 // 7 * 4 and p["tile_h"] == 2

@@ -14,19 +14,23 @@ def tm(fn, reps=20):
     for _ in range(reps): fn()
     e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps * 1e3
+if os.environ.get("SHAPES"):  # "n:C:K:H,..."
+    SHAPES = [tuple(int(v) for v in t.split(":")) for t in os.environ["SHAPES"].split(",")]
+KIDS = os.environ.get("KIDS", "A,B,E,P").split(",")
+POOLS = (False, True) if os.environ.get("POOL", "1") == "1" else (False,)
 for n, C, K, H in SHAPES:
     g = torch.Generator(device=dev); g.manual_seed(1)
     x = torch.rand(n, C, H + 2, H + 2, device=dev, generator=g)
     x = x * (torch.rand(x.shape, device=dev, generator=g) >= 0.7)
     w = torch.rand(K, C, 3, 3, device=dev, generator=g) - 0.5
     row = {"n": n, "C": C, "K": K, "H": H, "plan": sc.launch_plan(n, C, H + 2, H + 2, K, 3, 3, 1)["kernel"]}
-    for pool in (False, True):
-        for kid in ("A", "B", "E", "P"):
+    for pool in POOLS:
+        for kid in KIDS:
             if pool and kid == "B":
                 continue
             try:
-                f = (lambda: sc.pecr_conv_pool_batched(x, w, 1, sc.PoolConfig(2, 2, 2), fast=True, sync=False, kernel=kid)) if pool \
-                    else (lambda: sc.ecr_conv_batched(x, w, 1, fast=True, sync=False, kernel=kid))
+                f = (lambda: sc.pecr_conv_pool_batched(x, w, 1, sc.PoolConfig(2, 2, 2), fast=True, sync=False, kernel=int(kid) if kid.isdigit() else kid)) if pool \
+                    else (lambda: sc.ecr_conv_batched(x, w, 1, fast=True, sync=False, kernel=int(kid) if kid.isdigit() else kid))
                 row[("p" if pool else "") + kid] = round(tm(f), 1)
             except Exception as e:
                 row[("p" if pool else "") + kid] = str(e)[:20]
