@@ -68,7 +68,13 @@ struct WsCfg {
   // Measured (A/B, tools/gpu_ab2.sh): with R = 2 or 2-row tiles the border
   // cells carry so little work that branching always wins (conv5 2x7 -3.5%,
   // conv1_2 ECR -2.3%); 4x4 R = 4 tiles prefer predication above 25%.
-  static constexpr int SPARSE_PCT = (R <= 2 || TH <= 2) ? 100 : SCONV_SPARSE_PCT_WIDE;
+  // A 1x1 window is the opposite case on those tiles: one or two FFMA2 per cell
+  // costs less than the branch that would skip it, so only all-zero windows
+  // branch (GoogLeNet inception 5a 1x1 on 2x2 tiles: 101.6 -> 81.0 us,
+  // 4a.7: 55.4 -> 44.0 us; the 4x4 R = 4 config loses 4% that way and keeps
+  // the threshold).
+  static constexpr int SPARSE_PCT =
+      (R <= 2 || TH <= 2) ? (KH == 1 && KW == 1 ? 0 : 100) : SCONV_SPARSE_PCT_WIDE;
   static constexpr int PAIRS = WPC * NPOS / 2;
   static constexpr int PAIRS_PER_LANE = (PAIRS + 31) / 32;
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
