@@ -68,13 +68,15 @@ struct WsCfg {
   // Measured (A/B, tools/gpu_ab2.sh): with R = 2 or 2-row tiles the border
   // cells carry so little work that branching always wins (conv5 2x7 -3.5%,
   // conv1_2 ECR -2.3%); 4x4 R = 4 tiles prefer predication above 25%.
-  // A 1x1 window is the opposite case on those tiles: one or two FFMA2 per cell
-  // costs less than the branch that would skip it, so only all-zero windows
-  // branch (GoogLeNet inception 5a 1x1 on 2x2 tiles: 101.6 -> 81.0 us,
-  // 4a.7: 55.4 -> 44.0 us; the 4x4 R = 4 config loses 4% that way and keeps
-  // the threshold).
+  // 2x2 tiles and 1x1 windows are the opposite case: a cell feeds at most
+  // four outputs (one for 1x1), so its one to eight FFMA2 cost less than the
+  // branch that would skip it, and only all-zero windows branch.  Measured:
+  // inception 5a 1x1 on 2x2 tiles 101.6 -> 81.0 us, 4a.7 55.4 -> 44.0 us;
+  // 3x3 on 2x2 tiles: VGG conv4_2 at batch 1 164.6 -> 140.5 us, AlexNet conv4
+  // 102.5 -> 91.3 us, stride 3 conv4_2 1006 -> 913 us, stride 2 -3...-4%
+  // (the 4x4 R = 4 1x1 config loses 4% that way and keeps the threshold).
   static constexpr int SPARSE_PCT =
-      (R <= 2 || TH <= 2) ? (KH == 1 && KW == 1 ? 0 : 100) : SCONV_SPARSE_PCT_WIDE;
+      (TH == 2 && TW == 2) ? 0 : (R <= 2 || TH <= 2) ? (KH == 1 && KW == 1 ? 0 : 100) : SCONV_SPARSE_PCT_WIDE;
   static constexpr int PAIRS = WPC * NPOS / 2;
   static constexpr int PAIRS_PER_LANE = (PAIRS + 31) / 32;
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
