@@ -69,8 +69,10 @@ typedef enum {
  * network's launches in a CUDA graph on the first call and replay it while
  * the arguments (pointers, shapes, layers, flags) stay the same. */
 #define SCONV_F_GRAPH (1u << 4)
-/* Force one tiled kernel configuration (testing / tuning only; ignored when
- * the shape is not tileable): 1..6 = v2 TiledCfg1..6, 'A'..'G' = v3 WsA..G.
+/* Force one tiled kernel configuration (testing / tuning only): 1..6 = v2
+ * TiledCfg1..6 (ignored when the shape is not a 3x3 stride-1 tile);
+ * 'A'..'L', 'N'..'Q' = v3 WsA..WsQ (csrc/reg_v3.inc; SCONV_ERR_ARG when the
+ * config does not fit the window / stride); 'M' = the small-C kernel.
  * 0 (default) lets the launch layer pick. */
 #define SCONV_F_KERNEL(id) (((unsigned)(id) & 0xffu) << 8)
 
