@@ -11,7 +11,9 @@
 // private 48-float shared-memory slot, and runs the same per-channel body as
 // v2/v3 (ecr_body.cuh: ballot compaction + warp-uniform zero skip, terms of
 // each output in (c, i, j) order, so EXACT stays bit-identical).  No
-// __syncthreads anywhere; <= 85 registers -> 6 warps per scheduler.
+// __syncthreads in the channel loop.  ECR: 64 registers (16-20 B of spills), 4 CTAs =
+// 8 warps per scheduler: conv1_1 345 -> 333 us vs 3 CTAs at <= 80 registers;
+// PECR keeps 3 CTAs (its pool epilogue spills ~100 B at 64).
 #pragma once
 
 #include "common.cuh"
@@ -29,7 +31,7 @@ struct SmallCArgs {
 };
 
 template <int P, bool FAST>
-__global__ void __launch_bounds__(256, 3) ecr_smallc_kernel(const SmallCArgs a) {
+__global__ void __launch_bounds__(256, P == 0 ? 4 : 3) ecr_smallc_kernel(const SmallCArgs a) {
   constexpr int TH = 4, TW = 4, R = 2, KT = 64, WPH = 6, WPW = 6, PITCH = 8;
   __shared__ __align__(16) float win[8][WPH * PITCH];
   const int warp = __shfl_sync(kFull, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
