@@ -13,7 +13,14 @@ Inputs are device resident when `value` is timed; `e2e` runs the same step
 through the C ABI with pinned host buffers (H2D + kernel + D2H per layer).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--sparsity S] [--exact] [--sweep] [--no-cudnn]
+                    [--sparsity S] [--exact] [--global-batch 512] [--no-sweep] [--no-cudnn]
+
+The line also carries the per-layer roofline (`layers`), cuDNN on the same
+inputs, the sparsity sweep 0.5-0.95 (`sweep`), e2e through the C ABI with
+host buffers, the reference CPU path on this host (`cpu_baseline`, with a
+check of our outputs against the reference's own) and the multi-layer
+on-device forward.  `--global-batch 512` is BASELINE config 5: a fixed global
+batch split over the ranks by sconv_shard (strong scaling).
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the reference's own
 CPU implementation (oracle/_ref, built from /root/reference/proj/src) on the
@@ -33,28 +40,12 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# VGG-19 conv layers: (name, C, K, H_out, pooled?)  -- SURVEY.md 8(d)
-VGG19 = [
-    ("conv1_1", 3, 64, 224, False), ("conv1_2", 64, 64, 224, True),
-    ("conv2_1", 64, 128, 112, False), ("conv2_2", 128, 128, 112, True),
-    ("conv3_1", 128, 256, 56, False), ("conv3_2", 256, 256, 56, False),
-    ("conv3_3", 256, 256, 56, False), ("conv3_4", 256, 256, 56, True),
-    ("conv4_1", 256, 512, 28, False), ("conv4_2", 512, 512, 28, False),
-    ("conv4_3", 512, 512, 28, False), ("conv4_4", 512, 512, 28, True),
-    ("conv5_1", 512, 512, 14, False), ("conv5_2", 512, 512, 14, False),
-    ("conv5_3", 512, 512, 14, False), ("conv5_4", 512, 512, 14, True),
-]
+from paper_1909_09927_b200.workloads import (SWEEP, VGG19, filt_seed, map_seed,  # noqa: E402,F401
+                                              vgg_filters, vgg_maps)
+
 BATCH = 64
 METRIC = "ECR conv / PECR conv+pool µs per VGG-19 layer; achieved GB/s vs HBM peak"
 UNIT = "us/layer"
-
-
-def map_seed(l, n):
-    return 1_000_000 * (l + 1) + n
-
-
-def filt_seed(l, k):
-    return 1_000_000 * (l + 1) + 500_000 + k
 
 
 def peaks():
@@ -132,57 +123,64 @@ def cpu_lib():
     return oracle.c_oracle(), "port"
 
 
-def cpu_sample(lib, kind, step: int, filters_per_layer: int = 1):
-    """Time ecr_convert+ecr_spmv_conv (or pecr_convert+pecr_conv_pool) for 1
-    image x `filters_per_layer` filters per VGG-19 layer, as cmd_sweep times
-    it (tools/sparseconv_main.cpp:365-368).  Returns per-layer seconds per
-    (image, filter) and the total sample seconds."""
+def cpu_run(lib, kind, l, image, ks, workers, sparsity=0.7):
+    """ecr_convert+ecr_spmv_conv (or pecr_convert+pecr_conv_pool) of one image
+    by filters `ks` of layer l, as cmd_sweep times them per filter
+    (tools/sparseconv_main.cpp:365-368).  Returns (seconds, outputs [len(ks), ...])."""
     import numpy as np
-    workers = os.cpu_count() or 1
-    per = {}
-    total = 0.0
+    name, C, K, H, pooled = VGG19[l]
+    x = vgg_maps(l, [image], sparsity)
+    w = vgg_filters(l, ks)
+    kw = {"workers": workers} if kind == "reference" else {}
+    t0 = time.perf_counter()
+    if pooled:
+        y, _ = lib.pecr_conv(x, w, 1, 2, 2, 2, 0, **kw)
+    else:
+        y, _ = lib.ecr_conv(x, w, 1, **kw)
+    return time.perf_counter() - t0, np.asarray(y[0])
+
+
+def cpu_layer_us(lib, kind, image, filters, groups, workers, offset=0):
+    """Per-layer µs of the full layer (K filters x 64 images) extrapolated from
+    `groups` timed groups of `filters` filters each (median of the groups'
+    per-filter time: the reference spawns its worker threads per call, so
+    single groups are noisy).  Returns ({layer: us}, sample seconds, outputs of
+    the first group {layer: (ks, y)})."""
+    per, outs, total = {}, {}, 0.0
     for l, (name, C, K, H, pooled) in enumerate(VGG19):
-        x = lib.generate(H + 2, H + 2, C, 0.7, map_seed(l, step % BATCH))[None]
-        ks = [(step * filters_per_layer + j) % K for j in range(filters_per_layer)]
-        w = np.stack([lib.generate(3, 3, C, 0.0, filt_seed(l, k)) for k in ks]) - np.float32(0.5)
-        t0 = time.perf_counter()
-        if kind == "reference":
-            if pooled:
-                lib.pecr_conv(x, w, 1, 2, 2, 2, 0, workers=workers)
-            else:
-                lib.ecr_conv(x, w, 1, workers=workers)
-        else:
-            if pooled:
-                lib.pecr_conv(x, w, 1, 2, 2, 2, 0)
-            else:
-                lib.ecr_conv(x, w, 1)
-        dt = time.perf_counter() - t0
-        per[name] = dt / len(ks)
-        total += dt
-    return per, total
+        times = []
+        for g in range(groups):
+            ks = [(offset + g * filters + j) % K for j in range(filters)]
+            dt, y = cpu_run(lib, kind, l, image, ks, workers)
+            if g == 0:
+                outs[name] = (ks, y)
+            times.append(dt / filters)
+            total += dt
+        per[name] = statistics.median(times) * K * BATCH * 1e6
+    return per, total, outs
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU path on the host cores, each
+    step 16 filters per layer (median of 4 groups of 4) of one image,
+    extrapolated to K filters x 64 images."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return 0
     lib, kind = cpu_lib()
     cores = (os.cpu_count() or 1) if kind == "reference" else 1
     for s in range(args.warmup):
-        cpu_sample(lib, kind, 1000 + s)
-    times = []
-    per_layer_acc = {n: 0.0 for n, *_ in VGG19}
+        cpu_layer_us(lib, kind, (1000 + s) % BATCH, 1, 1, cores, offset=s)
+    steps, per_layer = [], {n: [] for n, *_ in VGG19}
     for s in range(args.steps):
-        per, _ = cpu_sample(lib, kind, s, filters_per_layer=4)
-        # extrapolate the sample to the full layer: x K filters x 64 images
-        step_us = 0.0
-        for name, C, K, H, pooled in VGG19:
-            us = per[name] * K * BATCH * 1e6
-            per_layer_acc[name] += us
-            step_us += us
-        times.append(step_us)
-    step_us = statistics.mean(times)
+        per, _, _ = cpu_layer_us(lib, kind, s % BATCH, 4, 4, cores, offset=16 * s)
+        for n, v in per.items():
+            per_layer[n].append(v)
+        steps.append(sum(per.values()))
+    step_us = statistics.median(steps)
     value = step_us / len(VGG19)
+    sample = (f"per step: image (step mod 64) x 16 filters per layer (median of 4 groups of 4), "
+              f"extrapolated x K x 64; value = median over steps")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -190,19 +188,110 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (sconv::generate)",
         "config": {"workload": "VGG-19 16 conv layers (11 ECR + 5 PECR conv+pool), batch 64, "
                                "sparsity 0.7", "global_batch": BATCH, "sparsity": 0.7,
-                   "sample": "1 image x 4 filters per layer per step, extrapolated x K x 64"},
+                   "sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": "1 image x 4 filters per layer per step (extrapolated x K x 64)"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "layers_us": {n: v / args.steps for n, v in per_layer_acc.items()},
+        "layers_us": {n: statistics.median(v) for n, v in per_layer.items()},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def cpu_baseline_leg(outs_dev, fast, sc, torch):
+    """The `cpu_baseline` of the GPU arm (rank 0, N = 1): the reference on this
+    host's cores (all of them, and one), plus a check of our GPU outputs
+    against the reference's own outputs for the sampled (image, filter) pairs."""
+    import numpy as np
+    lib, kind = cpu_lib()
+    cores = (os.cpu_count() or 1) if kind == "reference" else 1
+    image = 1
+    cpu_layer_us(lib, kind, image, 1, 1, cores)  # warm
+    per, total, ref_outs = cpu_layer_us(lib, kind, image, 8, 3, cores)
+    per1, total1, _ = cpu_layer_us(lib, kind, image, 1, 1, 1, offset=7) if kind == "reference" \
+        else (per, 0.0, None)
+    # extrapolation check: conv5_1 with all K = 512 filters of the image
+    l51 = [n for n, *_ in VGG19].index("conv5_1")
+    K51 = VGG19[l51][2]
+    dt_full, _ = cpu_run(lib, kind, l51, image, list(range(K51)), cores)
+    full_us = dt_full * BATCH * 1e6
+    # accuracy against the reference's own fp32 outputs (same inputs)
+    worst, exact_ok = 0.0, True
+    for l, (name, C, K, H, pooled) in enumerate(VGG19):
+        ks, yr = ref_outs[name]
+        got = outs_dev[l][image, ks].double().cpu().numpy()
+        ref = yr.astype(np.float64)
+        worst = max(worst, float((np.abs(got - ref) / (1e-5 + 1e-5 * np.abs(ref))).max()))
+        x1 = torch.from_numpy(vgg_maps(l, [image], 0.7)).cuda()
+        w1 = torch.from_numpy(vgg_filters(l)).cuda()
+        if pooled:
+            ye = sc.pecr_conv_pool_batched(x1, w1, 1, sc.PoolConfig(2, 2, 2), fast=False)
+        else:
+            ye = sc.ecr_conv_batched(x1, w1, 1, fast=False)
+        e = ye[0, ks].cpu().numpy()
+        exact_ok = exact_ok and np.array_equal(e.view(np.uint32), yr.view(np.uint32))
+    nl = len(VGG19)
+    return {"value": sum(per.values()) / nl, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"image 1 x 8 filters per layer x 3 groups (median per-filter time, "
+                      f"{total:.1f} s), extrapolated x K x 64",
+            "layers_us": {n: round(v, 1) for n, v in per.items()},
+            "workers_1": {"value": sum(per1.values()) / nl, "cores": 1,
+                          "sample": f"image 1 x 1 filter per layer ({total1:.1f} s)"}
+            if kind == "reference" else None,
+            "extrapolation_check": {"layer": "conv5_1", "full_k_us": full_us,
+                                    "extrapolated_us": per["conv5_1"],
+                                    "ratio": per["conv5_1"] / full_us,
+                                    "what": "all 512 filters of image 1 timed (x 64 images) vs "
+                                            "the 8-filter-group extrapolation"},
+            "accuracy_vs_reference": {
+                "fast_max_ratio": round(worst, 4), "exact_bit_identical": bool(exact_ok),
+                "what": "our outputs (FAST: max |d| / (1e-5 + 1e-5|ref|), EXACT: bits) on the "
+                        "reference's own outputs for the sampled filters of image 1, all 16 "
+                        "layers; the reference here is " + kind}}
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def layer_call(sc, l, x, w, out, fast, sync=False, **kw):
+    name, C, K, H, pooled = VGG19[l]
+    if pooled:
+        return sc.pecr_conv_pool_batched(x, w, 1, sc.PoolConfig(2, 2, 2), fast=fast, out=out,
+                                         sync=sync, **kw)
+    return sc.ecr_conv_batched(x, w, 1, fast=fast, out=out, sync=sync, **kw)
+
+
+def cudnn_call(torch, l, x, w):
+    y = torch.nn.functional.conv2d(x, w)
+    if VGG19[l][4]:
+        y = torch.nn.functional.max_pool2d(torch.relu(y), 2)
+    return y
+
+
+def useful_macs(torch, x, K):
+    """K x sum over images and windows of the window's nonzero count
+    (== the reference's OpCount.multiplications summed over the K filters)."""
+    nz = (x != 0).to(torch.float32).sum(1, keepdim=True)
+    win = torch.nn.functional.conv2d(nz, torch.ones(1, 1, 3, 3, device=x.device))
+    return float(win.sum().item()) * K
+
+
+def time_fn(torch, stream, fn, reps=3, trials=1):
+    """Mean ms of `reps` back-to-back launches after one warm call (best of `trials`)."""
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    best = None
+    for _ in range(trials):
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / reps
+        best = t if best is None else min(best, t)
+    return best
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -210,11 +299,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sparsity", type=float, default=0.7)
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="BASELINE config 5: a fixed global batch (e.g. 512) split over the "
+                         "ranks by sconv_shard (strong scaling); default 64 images per GPU")
     ap.add_argument("--exact", action="store_true", help="EXACT (bit-exact) arithmetic")
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also sweep sparsity (side file)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the sparsity sweep")
     ap.add_argument("--no-forward", action="store_true", help="skip the multi-layer forward leg")
     ap.add_argument("--no-check", action="store_true",
                     help="skip the accuracy spot check (profiling runs: keeps cuDNN out of the launch list)")
@@ -241,86 +333,65 @@ def main():
     torch.backends.cudnn.benchmark = True
     fast = not args.exact
     sp = args.sparsity
+    strong = args.global_batch > 0
+    if strong:  # config 5: contiguous image shards of the fixed global batch (sconv_shard)
+        n0, n1, _, _ = sc.shard(args.global_batch, 1, world, rank)
+        images = list(range(n0, n1))
+    else:       # weak scaling: this rank's own 64 images
+        images = [rank * BATCH + n for n in range(BATCH)]
+    nimg = len(images)
+    global_batch = args.global_batch if strong else BATCH * world
 
-    # ---- inputs: this rank's 64 images per layer (weak scaling) ---------
+    # ---- inputs ------------------------------------------------------------
     t_gen = time.time()
     host_x, host_w, dev_x, dev_w, outs, macs = [], [], [], [], [], []
     for l, (name, C, K, H, pooled) in enumerate(VGG19):
-        seeds = [map_seed(l, rank * BATCH + n) for n in range(BATCH)]
-        hx = torch.empty((BATCH, C, H + 2, H + 2), dtype=torch.float32, pin_memory=True)
-        sc.generate_batch(seeds, H + 2, H + 2, C, sp, out=hx.numpy())
+        hx = torch.empty((nimg, C, H + 2, H + 2), dtype=torch.float32, pin_memory=True)
+        vgg_maps(l, images, sp, out=hx.numpy())
         hw = torch.empty((K, C, 3, 3), dtype=torch.float32, pin_memory=True)
-        sc.generate_batch([filt_seed(l, k) for k in range(K)], 3, 3, C, 0.0, out=hw.numpy())
-        hw -= 0.5
+        vgg_filters(l, out=hw.numpy())
         host_x.append(hx)
         host_w.append(hw)
         dx = hx.to(dev, non_blocking=True)
-        dw = hw.to(dev, non_blocking=True)
         dev_x.append(dx)
-        dev_w.append(dw)
+        dev_w.append(hw.to(dev, non_blocking=True))
         oh = H // 2 if pooled else H
-        outs.append(torch.empty((BATCH, K, oh, oh), dtype=torch.float32, device=dev))
-        # useful MACs = K * sum over images/windows of window nnz (== OpCount.multiplications)
-        nz = (dx != 0).to(torch.float32).sum(1, keepdim=True)
-        win = torch.nn.functional.conv2d(nz, torch.ones(1, 1, 3, 3, device=dev))
-        macs.append(float(win.sum().item()) * K)
+        outs.append(torch.empty((nimg, K, oh, oh), dtype=torch.float32, device=dev))
+        macs.append(useful_macs(torch, dx, K))
     torch.cuda.synchronize()
     t_gen = time.time() - t_gen
 
     ctx = sc.context(local)
     stream = torch.cuda.current_stream(dev)
-    pool_cfg = sc.PoolConfig(2, 2, 2, sc.PoolMode.kMax)
+    nl = len(VGG19)
 
     def layer(l):
-        name, C, K, H, pooled = VGG19[l]
-        if pooled:
-            sc.pecr_conv_pool_batched(dev_x[l], dev_w[l], 1, pool_cfg, fast=fast, out=outs[l],
-                                      sync=False)
-        else:
-            sc.ecr_conv_batched(dev_x[l], dev_w[l], 1, fast=fast, out=outs[l], sync=False)
+        layer_call(sc, l, dev_x[l], dev_w[l], outs[l], fast)
 
-    # Accuracy spot check at full size (images 0-1 of every layer) against a
-    # float64 convolution: the north-star bar |d| <= 1e-5 + 1e-5|ref| as a
-    # ratio (<= 1 passes) for our output and for cuDNN fp32 (TF32 off).  The
-    # reference's own fp32 sum also deviates from float64 (its order differs),
-    # so the ratio of the oracle itself sits near 1; tests/ pin the oracle.
-    max_rel = 0.0
-    acc_ratio = {"ours_vs_reference": 0.0, "cudnn_vs_reference": 0.0, "ours_vs_f64": 0.0,
-                 "cudnn_vs_f64": 0.0}
-    for l, (name, C, K, H, pooled) in enumerate(VGG19):
+    # Accuracy against float64 (images 0-1 of every layer): the north-star bar
+    # |d| <= 1e-5 + 1e-5|ref| as a ratio for our output and for cuDNN fp32
+    # (TF32 off).  (The check against the reference's own fp32 outputs is in
+    # cpu_baseline.accuracy_vs_reference.)
+    acc_ratio = {"ours_vs_f64": 0.0, "cudnn_vs_f64": 0.0}
+    for l in range(nl):
         layer(l)
         if args.no_check:
             continue
         x2 = dev_x[l][:2]
-        # the reference's own fp32 result: EXACT mode is bit-identical to it
-        # (tests/test_gpu_parity.py, full VGG shapes included)
-        if pooled:
-            refx = sc.pecr_conv_pool_batched(x2, dev_w[l], 1, pool_cfg, fast=False)
-        else:
-            refx = sc.ecr_conv_batched(x2, dev_w[l], 1, fast=False)
-        ref64 = torch.nn.functional.conv2d(x2.double(), dev_w[l].double())
-        ref32 = torch.nn.functional.conv2d(x2, dev_w[l])
-        if pooled:
-            ref64 = torch.nn.functional.max_pool2d(torch.relu(ref64), 2)
-            ref32 = torch.nn.functional.max_pool2d(torch.relu(ref32), 2)
-        got, cud, rx = outs[l][:2].double(), ref32.double(), refx.double()
-        for tag, ref in (("reference", rx), ("f64", ref64)):
-            tol = 1e-5 + 1e-5 * ref.abs()
-            acc_ratio["ours_vs_" + tag] = max(acc_ratio["ours_vs_" + tag],
-                                              ((got - ref).abs() / tol).max().item())
-            acc_ratio["cudnn_vs_" + tag] = max(acc_ratio["cudnn_vs_" + tag],
-                                               ((cud - ref).abs() / tol).max().item())
-        err = ((got - cud).abs() / (1e-3 + cud.abs())).max().item()
-        max_rel = max(max_rel, err)
+        ref64 = cudnn_call(torch, l, x2.double(), dev_w[l].double())
+        cud = cudnn_call(torch, l, x2, dev_w[l]).double()
+        got = outs[l][:2].double()
+        tol = 1e-5 + 1e-5 * ref64.abs()
+        acc_ratio["ours_vs_f64"] = max(acc_ratio["ours_vs_f64"], ((got - ref64).abs() / tol).max().item())
+        acc_ratio["cudnn_vs_f64"] = max(acc_ratio["cudnn_vs_f64"], ((cud - ref64).abs() / tol).max().item())
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        for l in range(len(VGG19)):
+        for l in range(nl):
             layer(l)
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, events per layer --------------------------
-    nl = len(VGG19)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(args.steps)]
     launches0 = ctx.launches
     if world > 1:
@@ -346,58 +417,58 @@ def main():
         total_ms = t.item()
     ms_per_step = total_ms / args.steps
 
-    # ---- roofline of the dominant kernel (the fused ECR/PECR kernel) ------
+    # ---- roofline: the dominant kernel, and every layer ---------------------
     pk = peaks()
+    clocks = clk.summary()
+    fp32_peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12  # TFLOP/s at max SM clock
     flops = [2 * m for m in macs]
     in_bytes = [x.numel() * 4 for x in dev_x]
     w_bytes = [w.numel() * 4 for w in dev_w]
     out_bytes = [o.numel() * 4 for o in outs]
     alg_bytes = [a + b + c for a, b, c in zip(in_bytes, w_bytes, out_bytes)]
-    clocks = clk.summary()
-    fp32_peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12  # TFLOP/s at max SM clock
-    achieved_tf = sum(flops) / (sum(layer_ms) * 1e-3) / 1e12
-    achieved_gbs = sum(alg_bytes) / (sum(layer_ms) * 1e-3) / 1e9
+    per_layer = {}
+    for l, (name, C, K, H, pooled) in enumerate(VGG19):
+        t = layer_ms[l] * 1e-3
+        tf, gbs = flops[l] / t / 1e12, alg_bytes[l] / t / 1e9
+        per_layer[name] = {"us": round(layer_ms[l] * 1e3, 1),
+                           "kernel": "PECR conv+ReLU+maxpool2x2" if pooled else "ECR conv",
+                           "useful_tflops": round(tf, 2), "fp32_frac": round(tf / fp32_peak, 4),
+                           "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / pk["hbm_gbs"], 4),
+                           "bound": "hbm" if flops[l] / alg_bytes[l] < fp32_peak * 1e3 / pk["hbm_gbs"]
+                           else "fp32"}
     dom = max(range(nl), key=lambda l: layer_ms[l])
+    dom_tf = flops[dom] / (layer_ms[dom] * 1e-3) / 1e12
+    step_tf = sum(flops) / (sum(layer_ms) * 1e-3) / 1e12
+    step_gbs = sum(alg_bytes) / (sum(layer_ms) * 1e-3) / 1e9
     traffic = None  # DRAM bytes of the dominant layer's launch, from the committed ncu capture
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
-            t = json.load(f).get(VGG19[dom][0])
-        if t:
-            traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
-    except Exception:
-        pass
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "traffic.json")) as f:
+                t = json.load(f).get(VGG19[dom][0])
+            if t:
+                traffic = {"bytes": t["dram_read_bytes"] + t["dram_write_bytes"],
+                           "src": f"profiles/{rnd}/traffic.json"}
+                break
+        except Exception:
+            pass
 
     # ---- cuDNN dense comparison (same inputs, same GPU) -------------------
     cudnn = {}
     if not args.no_cudnn:
-        def dense(l):
-            name, C, K, H, pooled = VGG19[l]
-            y = torch.nn.functional.conv2d(dev_x[l], dev_w[l])
-            if pooled:
-                y = torch.nn.functional.max_pool2d(torch.relu(y), 2)
-            return y
         for l in range(nl):
             for _ in range(2):
-                dense(l)
+                cudnn_call(torch, l, dev_x[l], dev_w[l])
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        per = []
-        for l in range(nl):  # best of 3 trials of 3 launches: cuDNN at its fastest
-            best = None
-            for _ in range(3):
-                e0.record(stream)
-                for _ in range(3):
-                    dense(l)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                t = e0.elapsed_time(e1) / 3
-                best = t if best is None else min(best, t)
-            per.append(best)
+        per = [time_fn(torch, stream, lambda l=l: cudnn_call(torch, l, dev_x[l], dev_w[l]),
+                       reps=3, trials=3) for l in range(nl)]
         cudnn = {"ms_per_step": sum(per), "us_per_layer": sum(per) * 1e3 / nl,
                  "layers_us": {VGG19[l][0]: per[l] * 1e3 for l in range(nl)},
                  "speedup_ours_vs_cudnn": sum(per) / ms_per_step,
+                 "layers_won": sum(1 for l in range(nl) if per[l] > layer_ms[l]),
                  "settings": "torch conv2d(padding=0)+relu+max_pool2d, fp32, TF32 off, "
                              "cudnn.benchmark=True, best of 3 trials per layer"}
+        for l in range(nl):
+            per_layer[VGG19[l][0]]["cudnn_us"] = round(per[l] * 1e3, 1)
 
     # ---- e2e through the C ABI with pinned host buffers --------------------
     e2e = None
@@ -412,13 +483,8 @@ def main():
             # owns a workspace and its H2D / compute / D2H ring, so layer l+1's
             # input copy overlaps layer l's compute and output copy), then one
             # synchronisation: every H2D and D2H byte is inside the step
-            for l, (name, C, K, H, pooled) in enumerate(VGG19):
-                if pooled:
-                    sc.pecr_conv_pool_batched(xs[l], ws[l], 1, pool_cfg, fast=fast, out=ys[l],
-                                              device=local, sync=False)
-                else:
-                    sc.ecr_conv_batched(xs[l], ws[l], 1, fast=fast, out=ys[l], device=local,
-                                        sync=False)
+            for l in range(nl):
+                layer_call(sc, l, xs[l], ws[l], ys[l], fast, device=local)
             sc.synchronize(local)
         for _ in range(3):  # sizes the per-call workspaces and the memory pool
             e2e_step()
@@ -436,76 +502,91 @@ def main():
             t = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = t.item()
-        h2d = sum(in_bytes) + sum(w_bytes)
-        d2h = sum(out_bytes)
-        e2e = {"value": e2e_ms * 1e3 / nl / world, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "ms_each_step": e2e_each,
+        ok = all(np.array_equal(ys[l][:2].view(np.uint32), outs[l][:2].cpu().numpy().view(np.uint32))
+                 for l in range(nl))
+        e2e_value = (e2e_ms * 1e3 / nl * BATCH / global_batch) if strong else (e2e_ms * 1e3 / nl / world)
+        e2e = {"value": e2e_value, "unit": UNIT,
+               "h2d_bytes_per_step": sum(in_bytes) + sum(w_bytes),
+               "d2h_bytes_per_step": sum(out_bytes), "ms_per_step": e2e_ms,
+               "ms_each_step": e2e_each, "same_bits_as_device_path": ok,
                "path": "sconv_cu_ecr_conv / sconv_cu_pecr_conv_pool with pinned host pointers, "
                        "SCONV_F_ASYNC per layer + one sconv_cu_synchronize per step"}
 
-    # ---- CPU reference sample on this host (rank 0 only, N=1 only) --------
+    # ---- CPU reference on this host (rank 0 only, N = 1 only) --------------
     cpu = None
-    if not args.no_cpu and rank == 0 and world == 1:
+    if not args.no_cpu and rank == 0 and world == 1 and not strong:
         try:
-            lib, kind = cpu_lib()
-            cpu_sample(lib, kind, 0)  # warm
-            per, total = cpu_sample(lib, kind, 1, filters_per_layer=48)  # ~10 s of CPU work
-            est_us = sum(per[n] * K * BATCH * 1e6 for n, C, K, H, p in VGG19)
-            cpu = {"value": est_us / nl, "unit": UNIT,
-                   "cores": (os.cpu_count() or 1) if kind == "reference" else 1, "kind": kind,
-                   "sample": f"1 image x 48 filters per layer ({total:.1f} s), extrapolated x K x 64",
-                   "speedup_ours_vs_cpu": (est_us / 1e3) / ms_per_step}
+            cpu = cpu_baseline_leg(outs, fast, sc, torch)
+            cpu["speedup_ours_vs_cpu"] = cpu["value"] / (ms_per_step * 1e3 / nl)
         except Exception as exc:  # the GPU number stands without it
-            cpu = {"value": None, "error": str(exc)[:200]}
+            cpu = {"value": None, "error": str(exc)[:300]}
 
-    if args.sweep and rank == 0:
-        sweep_side_file(sc, torch, dev, fast)
+    sweep = None
+    if not args.no_sweep and rank == 0 and world == 1 and not strong:
+        sweep = sweep_leg(sc, torch, dev, stream, fast, host_x, dev_x, dev_w, outs, images)
 
     fwd = None if args.no_forward else forward_side(sc, torch, dev, fast, rank)
 
-    value = ms_per_step * 1e3 / nl / world
+    # weak: per-GPU work fixed, value = step time / 16 layers / N (whole-job
+    # throughput in µs per layer-batch of 64); strong: the fixed global batch
+    if strong:
+        value = ms_per_step * 1e3 / nl * BATCH / global_batch
+    else:
+        value = ms_per_step * 1e3 / nl / world
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (sconv::generate, bit-identical to the reference generator)",
         "config": {
             "workload": "VGG-19 16 conv layers: 11 ECR conv + 5 PECR conv+ReLU+maxpool2x2, "
-                        "batch 64 per GPU, sparsity %.2f, valid 3x3 s1 on pre-padded inputs" % sp,
-            "global_batch": BATCH * world, "sparsity": sp, "parallelism": f"batch-shard x{world}",
+                        + (f"global batch {global_batch} sharded by image over {world} GPU(s)"
+                           if strong else "batch 64 per GPU")
+                        + ", sparsity %.2f, valid 3x3 s1 on pre-padded inputs" % sp,
+            "global_batch": global_batch, "images_this_rank": nimg, "sparsity": sp,
+            "parallelism": f"batch-shard x{world}",
             "arith": "FAST (FFMA, |d|<=1e-5+1e-5|ref|)" if fast else "EXACT (bit-exact)",
-            "l2": "inputs larger than L2: 2.8 GB of inputs per step, every layer's input is "
-                  "evicted by the other 15 layers' traffic before it is read again",
+            "l2": "inputs larger than L2: 2.8 GB of inputs per 64-image step, every layer's "
+                  "input is evicted by the other 15 layers' traffic before it is read again",
             "seeds": "map 1e6*(l+1)+n, filter 1e6*(l+1)+5e5+k, filters - 0.5",
+            "value_what": ("µs per layer per 64 images of the global batch (step time x 64 / "
+                           "global batch / 16)") if strong else
+                          "µs per layer per 64-image batch per GPU (step time / 16 / N)",
         },
-        "images_per_s": BATCH * world / (ms_per_step * 1e-3),
+        "images_per_s": global_batch / (ms_per_step * 1e-3),
         "layers_us": {VGG19[l][0]: layer_ms[l] * 1e3 for l in range(nl)},
+        "layers": per_layer,
         "roofline": {
-            "bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
-            "frac": achieved_tf / fp32_peak, "traffic": traffic,
-            "traffic_what": "dram__bytes_read+write of one launch of the dominant layer "
-                            "(profiles/r01/traffic.json) vs its algorithmic bytes "
-                            "dominant_layer_alg_bytes",
-            "dominant_layer_alg_bytes": alg_bytes[dom],
-            "what": "useful (nonzero) FLOPs of the fused ECR/PECR kernel over its event time; "
-                    "peak = FP32 FFMA 148 SM x 128 x 2 x sm_max_mhz (not in MEASURED_PEAKS)",
-            "hbm": {"achieved_gbs": achieved_gbs, "peak_gbs": pk["hbm_gbs"],
-                    "frac": achieved_gbs / pk["hbm_gbs"], "peak_src": pk["src"],
-                    "bytes": "compulsory: inputs + filters + outputs"},
+            "bound": "fp32", "achieved": dom_tf, "peak": fp32_peak, "unit": "TFLOP/s",
+            "frac": dom_tf / fp32_peak,
+            "traffic": traffic["bytes"] if traffic else None,
+            "traffic_src": traffic["src"] if traffic else None,
             "dominant_layer": VGG19[dom][0],
-            "dominant_layer_tflops": flops[dom] / (layer_ms[dom] * 1e-3) / 1e12,
+            "dominant_layer_alg_bytes": alg_bytes[dom],
+            "dominant_layer_useful_flop": flops[dom],
+            "what": "dominant launch (the slowest layer): useful (nonzero) FLOPs per launch "
+                    "(2 x K x sum of window nnz) over its CUDA-event time on the launching "
+                    "stream; peak = FP32 FFMA 148 SM x 128 x 2 x sm_max_mhz (not in "
+                    "MEASURED_PEAKS; tools/micro/ffma_rate.cu measured 92% of it); traffic = "
+                    "ncu dram bytes of that launch vs dominant_layer_alg_bytes",
+            "step_average": {"achieved": step_tf, "frac": step_tf / fp32_peak},
+            "hbm": {"achieved_gbs": step_gbs, "peak_gbs": pk["hbm_gbs"],
+                    "frac": step_gbs / pk["hbm_gbs"], "peak_src": pk["src"],
+                    "bytes": "compulsory: inputs + filters + outputs",
+                    "conv1_1_frac": per_layer["conv1_1"]["hbm_frac"]},
         },
         "useful_gflop_per_step": sum(flops) / 1e9,
-        "max_rel_err_vs_cudnn": max_rel,
         "accuracy": {k: round(v, 3) for k, v in acc_ratio.items()},
-        "accuracy_what": "max over all 16 layers (images 0-1) of |out - ref| / (1e-5 + 1e-5|ref|)"
-                         " with ref = the reference's fp32 result (our EXACT mode, bit-identical"
-                         " to it) or a float64 convolution; <= 1 meets the north-star bar",
+        "accuracy_what": "max over all 16 layers (images 0-1) of |out - f64| / (1e-5 + 1e-5|f64|) "
+                         "against a float64 convolution (<= 1 meets the bar against exact "
+                         "arithmetic; the bar proper is against the reference's fp32 result: "
+                         "cpu_baseline.accuracy_vs_reference)",
         "gpu_launches": launches,
         "clocks": clocks,
         "cudnn": cudnn or None,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "sweep": sweep,
         "forward": fwd,
         "setup_s": t_gen,
     }
@@ -514,6 +595,43 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def sweep_leg(sc, torch, dev, stream, fast, host_x, dev_x, dev_w, outs, images):
+    """BASELINE config 3: every layer at sparsity 0.5-0.95 on the reference
+    generator's inputs (the bench's own seeds, batch 64): our kernel in the
+    step's assignment (PECR conv+ReLU+pool on the 5 pooled layers, ECR on the
+    rest, plus ECR on the pooled layers), cuDNN on the same inputs, useful
+    TFLOP/s.  Overwrites the bench inputs (run after every other leg that
+    reads them)."""
+    nl = len(VGG19)
+    rows = {}
+    for s in SWEEP:
+        per, cud, tfs, ecr_pool = [], [], [], {}
+        for l, (name, C, K, H, pooled) in enumerate(VGG19):
+            vgg_maps(l, images, s, out=host_x[l].numpy())
+            dev_x[l].copy_(host_x[l], non_blocking=True)
+            m = useful_macs(torch, dev_x[l], K)
+            t = time_fn(torch, stream, lambda: layer_call(sc, l, dev_x[l], dev_w[l], outs[l], fast))
+            per.append(t)
+            cud.append(time_fn(torch, stream, lambda: cudnn_call(torch, l, dev_x[l], dev_w[l])))
+            tfs.append(2 * m / (t * 1e-3) / 1e12)
+            if pooled:
+                ecr_pool[name] = round(time_fn(torch, stream, lambda: sc.ecr_conv_batched(
+                    dev_x[l], dev_w[l], 1, fast=fast, sync=False)) * 1e3, 1)
+        rows[str(s)] = {
+            "ms_per_step": round(sum(per), 3), "us_per_layer": round(sum(per) * 1e3 / nl, 1),
+            "cudnn_ms_per_step": round(sum(cud), 3),
+            "speedup_vs_cudnn": round(sum(cud) / sum(per), 3),
+            "layers_won_vs_cudnn": sum(1 for a, b in zip(per, cud) if a < b),
+            "layers_us": {VGG19[l][0]: round(per[l] * 1e3, 1) for l in range(nl)},
+            "cudnn_layers_us": {VGG19[l][0]: round(cud[l] * 1e3, 1) for l in range(nl)},
+            "useful_tflops": {VGG19[l][0]: round(tfs[l], 2) for l in range(nl)},
+            "ecr_on_pooled_layers_us": ecr_pool,
+        }
+    return {"what": "per sparsity: our step (11 ECR + 5 PECR) vs cuDNN conv(+ReLU+pool), batch 64, "
+                    "reference-generator inputs; 3 launches per layer after one warm call",
+            "by_sparsity": rows}
 
 
 # VGG-19 on valid convolutions (the reference's forward() has no padding): a
@@ -586,50 +704,6 @@ def forward_side(sc, torch, dev, fast, rank):
             "output_nonzero_frac": nz,
             "batch1_ms": lat,
             "path": "sconv_cu_forward (one call, device pointers)"}
-
-
-def sweep_side_file(sc, torch, dev, fast):
-    """Sparsity sweep per layer (ECR for all 16 layers, PECR for the pooled
-    ones), written to profiles/sweep_latest.json (not the bench line)."""
-    res = []
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for s in (0.5, 0.6, 0.7, 0.8, 0.9, 0.95):
-        for l, (name, C, K, H, pooled) in enumerate(VGG19):
-            g = torch.Generator(device=dev)
-            g.manual_seed(l)
-            x = torch.rand(BATCH, C, H + 2, H + 2, device=dev, generator=g)
-            x = x * (torch.rand(x.shape, device=dev, generator=g) >= s)
-            w = torch.rand(K, C, 3, 3, device=dev, generator=g) - 0.5
-            macs = float(torch.nn.functional.conv2d((x != 0).float().sum(1, keepdim=True),
-                                                    torch.ones(1, 1, 3, 3, device=dev)).sum()) * K
-            row = {"sparsity": s, "layer": name}
-            for tag, fn in (("ecr", lambda: sc.ecr_conv_batched(x, w, 1, fast=fast, sync=False)),
-                            ("cudnn", lambda: torch.nn.functional.conv2d(x, w))):
-                fn()
-                ev0.record()
-                for _ in range(3):
-                    fn()
-                ev1.record()
-                torch.cuda.synchronize()
-                row[tag + "_us"] = ev0.elapsed_time(ev1) / 3 * 1e3
-            if pooled:
-                pc = sc.PoolConfig(2, 2, 2)
-                for tag, fn in (("pecr", lambda: sc.pecr_conv_pool_batched(x, w, 1, pc, fast=fast,
-                                                                           sync=False)),
-                                ("cudnn_pool", lambda: torch.nn.functional.max_pool2d(
-                                    torch.relu(torch.nn.functional.conv2d(x, w)), 2))):
-                    fn()
-                    ev0.record()
-                    for _ in range(3):
-                        fn()
-                    ev1.record()
-                    torch.cuda.synchronize()
-                    row[tag + "_us"] = ev0.elapsed_time(ev1) / 3 * 1e3
-            row["useful_tflops"] = 2 * macs / (row["ecr_us"] * 1e-6) / 1e12
-            res.append(row)
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    with open(os.path.join(ROOT, "profiles", "sweep_latest.json"), "w") as f:
-        json.dump(res, f, indent=1)
 
 
 if __name__ == "__main__":

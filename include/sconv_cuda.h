@@ -54,11 +54,13 @@ typedef enum {
 #define SCONV_F_EXACT 0u
 #define SCONV_F_FAST (1u << 0)
 /* Every tensor pointer is a device pointer on the context's device (no
- * host<->device copies).  Without it all pointers are host pointers. */
+ * host<->device copies).  Without it all pointers are host pointers.  Device
+ * maps x and outputs y must be 16-byte aligned (SCONV_ERR_ARG otherwise: the
+ * kernels move 8- and 16-byte vectors). */
 #define SCONV_F_DEVICE (1u << 1)
 /* Return right after enqueueing (no synchronisation); counters must be NULL.
  * With SCONV_F_DEVICE the work is ordered on the context stream.  With host
- * pointers the call owns one of 16 rotating workspaces and its own
+ * pointers the call owns one of 6 rotating workspaces and its own
  * H2D / compute / D2H ring, so consecutive calls overlap their transfers;
  * the inputs must stay unchanged and the outputs unread until
  * sconv_cu_synchronize(ctx) (use pinned memory for the copies to overlap). */
@@ -69,6 +71,13 @@ typedef enum {
  * network's launches in a CUDA graph on the first call and replay it while
  * the arguments (pointers, shapes, layers, flags) stay the same. */
 #define SCONV_F_GRAPH (1u << 4)
+/* The caller promises that the filter values at this filters pointer (same
+ * pointer, same K x C x kh x kw) do not change between calls, as for the
+ * layer weights of an inference network: the context keeps the kernels'
+ * re-laid-out copy ([C][kh*kw][Kp], plus the filters' device copy for host
+ * pointers) and reuses it instead of copying / transposing every call.
+ * sconv_cu_release_filters drops the cached copies. */
+#define SCONV_F_CACHE_FILTERS (1u << 5)
 /* Force one tiled kernel configuration (testing / tuning only): 1..6 = v2
  * TiledCfg1..6 (ignored when the shape is not a 3x3 stride-1 tile);
  * 'A'..'L', 'N'..'Q' = v3 WsA..WsQ (csrc/reg_v3.inc; SCONV_ERR_ARG when the
@@ -97,6 +106,9 @@ int sconv_cu_synchronize(sconv_cu_ctx* ctx);
 const char* sconv_cu_last_error(const sconv_cu_ctx* ctx);
 /* Number of kernels this context has launched (evidence counter). */
 uint64_t sconv_cu_launch_count(const sconv_cu_ctx* ctx);
+/* Drop every filter copy kept for SCONV_F_CACHE_FILTERS calls (waits for the
+ * context's work first). */
+int sconv_cu_release_filters(sconv_cu_ctx* ctx);
 
 /* ---- geometry (host only) ---------------------------------------------- */
 /* conv_output_dims, src/tensor.cpp:44-55. */

@@ -27,6 +27,7 @@ SYMBOLS = (
     "sconv_cu_pecr_conv_pool_multi", "sconv_generate", "sconv_generate_batch", "sconv_checksum",
     "sconv_cu_forward", "sconv_cu_forward_dims", "sconv_io_last_error", "sconv_map_file_dims",
     "sconv_load_map", "sconv_save_map", "sconv_load_maps", "sconv_cu_window_nnz",
+    "sconv_cu_release_filters",
 )
 
 F_EXACT = 0
@@ -35,6 +36,7 @@ F_DEVICE = 1 << 1
 F_ASYNC = 1 << 2
 F_GENERIC = 1 << 3
 F_GRAPH = 1 << 4
+F_CACHE_FILTERS = 1 << 5
 
 
 def F_KERNEL(kid) -> int:
@@ -89,6 +91,7 @@ def lib() -> C.CDLL:
     L.sconv_cu_last_error.restype = C.c_char_p
     L.sconv_cu_launch_count.argtypes = [_vp]
     L.sconv_cu_launch_count.restype = C.c_uint64
+    L.sconv_cu_release_filters.argtypes = [_vp]
     L.sconv_conv_output_dims.argtypes = [_i] * 5 + [C.POINTER(_i)] * 2
     L.sconv_pecr_pack_count.argtypes = [_i] * 5 + [C.POINTER(_i)]
     L.sconv_cu_plan.argtypes = [_i] * 11 + [C.c_uint, C.POINTER(LaunchPlan)]
@@ -163,6 +166,10 @@ class Context:
             self._inflight = []
         self._inflight.extend(arrays)
 
+    def release_filters(self) -> None:
+        """Drop the filter copies kept for cache_filters=True calls."""
+        check(lib().sconv_cu_release_filters(self.handle), self.handle)
+
     @property
     def launches(self) -> int:
         return int(lib().sconv_cu_launch_count(self.handle))
@@ -179,11 +186,14 @@ class Context:
             pass
 
 
-_contexts: dict[int, Context] = {}
+_contexts: dict[tuple[int, int], Context] = {}
 
 
-def context(device: int = 0) -> Context:
-    ctx = _contexts.get(device)
+def context(device: int = 0, slot: int = 0) -> Context:
+    """The process-wide context `slot` of `device` (slot 0 is the default one;
+    further slots are independent contexts on the same device, each with its
+    own stream and workspace, e.g. for sconv_cu_*_multi on one GPU)."""
+    ctx = _contexts.get((device, slot))
     if ctx is None:
-        ctx = _contexts[device] = Context(device)
+        ctx = _contexts[(device, slot)] = Context(device)
     return ctx

@@ -472,10 +472,19 @@ def _is_torch_cuda(t) -> bool:
     return hasattr(t, "is_cuda") and bool(getattr(t, "is_cuda"))
 
 
+def _aligned16(t):
+    """The device entries take 16-byte aligned maps (SCONV_F_DEVICE); a view
+    at an odd storage offset is copied once instead of faulting."""
+    return t if t.data_ptr() % 16 == 0 else t.clone()
+
+
 def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, counters,
-             device: Optional[int], generic: bool, out, sync: bool, kernel=0):
+             device: Optional[int], generic: bool, out, sync: bool, kernel=0,
+             cache_filters: bool = False):
     L = nat.lib()
     flags = (nat.F_FAST if fast else 0) | (nat.F_GENERIC if generic else 0)
+    if cache_filters:
+        flags |= nat.F_CACHE_FILTERS
     if kernel:
         flags |= nat.F_KERNEL(kernel)
     if _is_torch_cuda(x):
@@ -483,7 +492,7 @@ def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, co
         if not (_is_torch_cuda(filters) and x.dtype == torch.float32 and filters.dtype == torch.float32):
             raise ShapeError("x and filters must both be float32 CUDA tensors")
         dev = x.device.index if device is None else device
-        x = x.contiguous()
+        x = _aligned16(x.contiguous())
         filters = filters.contiguous()
         N, Cc, H, W = x.shape
         K, Cf, kh, kw = filters.shape
@@ -496,10 +505,13 @@ def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, co
             pw = pecr_pack_count(W, kw, stride, pool[0], pool[2])
             ph = pecr_pack_count(H, kh, stride, pool[1], pool[2])
             shape = (N, K, ph, pw)
+        user_out = None
         if out is None:
             out = torch.empty(shape, dtype=torch.float32, device=x.device)
         elif tuple(out.shape) != shape or not out.is_contiguous():
             raise ShapeError("out has the wrong shape")
+        elif out.data_ptr() % 16:
+            user_out, out = out, torch.empty(shape, dtype=torch.float32, device=x.device)
         ctx = nat.context(dev)
         ctx.set_stream(torch.cuda.current_stream(x.device).cuda_stream)
         flags |= nat.F_DEVICE
@@ -507,6 +519,7 @@ def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, co
             flags |= nat.F_ASYNC
         xp, wp, yp = x.data_ptr(), filters.data_ptr(), out.data_ptr()
     else:
+        user_out = None
         x = np.ascontiguousarray(x, np.float32)
         filters = np.ascontiguousarray(filters, np.float32)
         N, Cc, H, W = x.shape
@@ -543,6 +556,9 @@ def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, co
     nat.check(st, ctx.handle)
     if counters is not None:
         counters.merge(OpCount(m.value, a.value))
+    if _is_torch_cuda(x) and user_out is not None:
+        user_out.copy_(out)
+        return user_out
     return out
 
 
@@ -554,7 +570,8 @@ def synchronize(device: int = 0) -> None:
 
 def ecr_conv_batched(x, filters, stride: int = 1, *, fast: bool = False,
                      counters: Optional[OpCount] = None, device: Optional[int] = None,
-                     generic: bool = False, out=None, sync: bool = True, kernel=0):
+                     generic: bool = False, out=None, sync: bool = True, kernel=0,
+                     cache_filters: bool = False):
     """Fused ECR convolution of x [N,C,H,W] by filters [K,C,kh,kw] -> [N,K,oh,ow].
 
     Equivalent to multichannel_conv(map, filters, {stride}, Method::kEcr) per
@@ -563,18 +580,82 @@ def ecr_conv_batched(x, filters, stride: int = 1, *, fast: bool = False,
     returns after enqueueing (numpy: pinned buffers overlap; call
     synchronize() before reading out).  `kernel`
     forces a tiled configuration (testing / tuning; SCONV_F_KERNEL).
+    `cache_filters` (SCONV_F_CACHE_FILTERS) promises the filter values behind
+    this buffer never change: the context keeps their device re-layout.
     """
     return _batched("ecr", x, filters, stride, None, 0, fast, counters, device, generic, out,
-                    sync, kernel)
+                    sync, kernel, cache_filters)
 
 
 def pecr_conv_pool_batched(x, filters, stride: int = 1, pool: PoolConfig = PoolConfig(2, 2, 2),
                            *, fast: bool = False, counters: Optional[OpCount] = None,
                            device: Optional[int] = None, generic: bool = False, out=None,
-                           sync: bool = True, kernel=0):
+                           sync: bool = True, kernel=0, cache_filters: bool = False):
     """Fused conv + ReLU + pooling (forward's fused branch, pipeline.cpp:249-264)."""
     return _batched("pecr", x, filters, stride, (pool.width, pool.height, pool.stride),
-                    int(pool.mode), fast, counters, device, generic, out, sync, kernel)
+                    int(pool.mode), fast, counters, device, generic, out, sync, kernel,
+                    cache_filters)
+
+
+def _multi(kind: str, x, filters, stride: int, pool, mode: int, devices: Sequence[int],
+           fast: bool, counters: Optional[OpCount]):
+    L = nat.lib()
+    x = np.ascontiguousarray(x, np.float32)
+    filters = np.ascontiguousarray(filters, np.float32)
+    N, Cc, H, W = x.shape
+    K, Cf, kh, kw = filters.shape
+    if Cf != Cc:
+        raise ShapeError(f"filter channels {Cf} != map channels {Cc}")
+    if not devices:
+        raise ConfigError("no devices")
+    # one context per entry: a device listed twice gets two contexts (slots)
+    seen: dict[int, int] = {}
+    ctxs = []
+    for d in devices:
+        ctxs.append(nat.context(d, seen.get(d, 0)))
+        seen[d] = seen.get(d, 0) + 1
+    for c in ctxs:
+        c.use_own_stream()
+    arr = (C.c_void_p * len(ctxs))(*[c.handle for c in ctxs])
+    if kind == "ecr":
+        od = conv_output_dims(W, H, kw, kh, stride)
+        out = np.empty((N, K, od.height, od.width), np.float32)
+    else:
+        pw = pecr_pack_count(W, kw, stride, pool[0], pool[2])
+        ph = pecr_pack_count(H, kh, stride, pool[1], pool[2])
+        out = np.empty((N, K, ph, pw), np.float32)
+    m, a = C.c_uint64(0), C.c_uint64(0)
+    mp = C.byref(m) if counters is not None else None
+    ap = C.byref(a) if counters is not None else None
+    flags = nat.F_FAST if fast else 0
+    if kind == "ecr":
+        st = L.sconv_cu_ecr_conv_multi(arr, len(ctxs), _ptr(x), N, Cc, H, W, _ptr(filters), K, kh,
+                                       kw, stride, _ptr(out), mp, ap, flags)
+    else:
+        st = L.sconv_cu_pecr_conv_pool_multi(arr, len(ctxs), _ptr(x), N, Cc, H, W, _ptr(filters),
+                                             K, kh, kw, stride, pool[0], pool[1], pool[2],
+                                             int(mode), _ptr(out), mp, ap, flags)
+    nat.check(st, None)
+    if counters is not None:
+        counters.merge(OpCount(m.value, a.value))
+    return out
+
+
+def ecr_conv_multi(x, filters, stride: int = 1, *, devices: Sequence[int] = (0,),
+                   fast: bool = False, counters: Optional[OpCount] = None) -> np.ndarray:
+    """ECR convolution sharded over several contexts (sconv_cu_ecr_conv_multi):
+    each entry of `devices` gets a contiguous shard of the images (or, with
+    fewer images than entries, of the filters) -- dispatch over GPUs
+    (include/sconv/exec.hpp:57-120).  Host arrays in, host array out."""
+    return _multi("ecr", x, filters, stride, None, 0, devices, fast, counters)
+
+
+def pecr_conv_pool_multi(x, filters, stride: int = 1, pool: PoolConfig = PoolConfig(2, 2, 2), *,
+                         devices: Sequence[int] = (0,), fast: bool = False,
+                         counters: Optional[OpCount] = None) -> np.ndarray:
+    """Fused conv + ReLU + pool sharded over contexts (sconv_cu_pecr_conv_pool_multi)."""
+    return _multi("pecr", x, filters, stride, (pool.width, pool.height, pool.stride),
+                  int(pool.mode), devices, fast, counters)
 
 
 def multichannel_conv(map: FeatureMap, filters: Sequence[Filter], cfg: ConvConfig,
@@ -729,7 +810,7 @@ def forward_batched(x, layers: Sequence[dict], method: Method = Method.kPecr, *,
     torch_in = _is_torch_cuda(x)
     if torch_in:
         import torch
-        x = x.contiguous()
+        x = _aligned16(x.contiguous())
         ws = [lay["filters"].contiguous() for lay in layers]
         dev = x.device.index if device is None else device
         N, Cc, H, W = x.shape
@@ -773,6 +854,8 @@ def forward_batched(x, layers: Sequence[dict], method: Method = Method.kPecr, *,
         out = mk((N, oc.value, oh.value, ow.value))
     elif tuple(out.shape) != (N, oc.value, oh.value, ow.value):
         raise ShapeError("out has the wrong shape")
+    elif torch_in and out.data_ptr() % 16:
+        raise ShapeError("out must be 16-byte aligned (SCONV_F_DEVICE)")
     lo = [mk((N, k, ph, pw)) for k, _, _, ph, pw in dims] if layer_outputs else None
     fused = [int(method) == Method.kPecr and cf["pool"] is not None and cf["relu"] for cf in cfg]
     co = ([None if fz else mk((N, k, h2, w2)) for fz, (k, h2, w2, _, _) in zip(fused, dims)]

@@ -3,17 +3,48 @@
 // helpers, and the v2 / v3 kernel registries (reg_v2.cu, reg_v3_*.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "kernels/ecr_tiled.cuh"
 #include "kernels/ecr_ws.cuh"
 #include "sconv_cuda.h"
 
+// A filter slab kept for SCONV_F_CACHE_FILTERS calls: keyed by the caller's
+// pointer and shape; `dev` is the device copy (host-pointer calls) and `wt`
+// the kernels' [C][kh*kw][Kp] re-layout.
+struct sconv_filter_entry {
+  const float* src;
+  bool host;
+  int k, c, kk, kp;
+  float* dev;
+  float* wt;
+};
+// Encoded TMA descriptors of the weight slabs (reg_v3.inc), keyed by address
+// and box: encoding is pure host work, repeated otherwise on every launch.
+struct sconv_tmap_entry {
+  const float* wt;
+  int c, kk, kp, kt, cc;
+  CUtensorMap map;
+};
+
 struct sconv_cu_ctx {
   int device = 0;
+  // Stream-ordered allocations of this context (async host workspaces) come
+  // from its own pool, so raising the pool's release threshold does not
+  // change the device's default pool for the host application.
+  cudaMemPool_t pool = nullptr;
+  // Bumped whenever a workspace the captured forward graph may point into
+  // (ws, hws, fwd) is reallocated: the graph is re-captured instead of
+  // replaying stale addresses.
+  uint64_t mem_gen = 0;
+  uint64_t fwd_gen = 0;
+  std::vector<sconv_filter_entry> fcache;
+  std::vector<sconv_tmap_entry> tmaps;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   std::string err;

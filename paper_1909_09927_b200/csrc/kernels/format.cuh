@@ -218,7 +218,11 @@ __global__ void pecr_check_kernel(const PecrPoolArgs a, int64_t total) {
     if (a.index[q] < 0 || a.index[q] >= a.cap) atomicOr(a.bad, 1);
 }
 
+// Both pool kernels run after pecr_check_kernel on device formats: a format
+// it flagged is never read (the reference throws FormatError before any
+// computation, src/pecr.cpp:24-58), so a bad index cannot fault the context.
 __global__ void pecr_pool_exact_kernel(const PecrPoolArgs a) {
+  if (*a.bad) return;  // uniform across the grid
   const int pk = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long muls = 0, adds = 0;
   if (pk < a.npacks) {
@@ -241,6 +245,7 @@ __global__ void pecr_pool_exact_kernel(const PecrPoolArgs a) {
 }
 
 __global__ void pecr_pool_fast_kernel(const PecrPoolArgs a) {
+  if (*a.bad) return;
   const int lane = threadIdx.x & 31;
   const int pk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   unsigned long long muls = 0, adds = 0;

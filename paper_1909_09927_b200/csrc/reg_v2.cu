@@ -2,6 +2,7 @@
 // configurations, selection and launch.  Its own translation unit so the
 // template instantiations compile in parallel with the rest of the library.
 #include <cstdlib>
+#include <mutex>
 
 #include "host/internal.h"
 
@@ -31,12 +32,12 @@ constexpr int min_blocks() {
 template <class Cfg, bool FAST, bool NOSKIP = false>
 int launch_tiled_cfg(sconv_cu_ctx* ctx, const TiledArgs& a, int N) {
   auto kern = ecr_tiled_kernel<Cfg, FAST, min_blocks<Cfg>(), NOSKIP>;
-  static bool attr_done[64] = {};
-  const int slot = ctx->device & 63;
-  if (!attr_done[slot]) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_done[slot] = true;
-  }
+  static std::once_flag attr_once[64];  // per (instantiation, device), thread-safe
+  cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once[ctx->device & 63], [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  });
+  CK(attr_err);
   const int tiles_y = (a.OH + Cfg::OTH - 1) / Cfg::OTH;
   const int tiles_x = (a.OW + Cfg::OTW - 1) / Cfg::OTW;
   TiledArgs b = a;

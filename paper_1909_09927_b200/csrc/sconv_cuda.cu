@@ -90,6 +90,7 @@ struct Arena {
     if (total > cap_) {
       size_t cap = std::max(total, cap_ + cap_ / 2);
       if (host >= 0) cap = ctx->hws_max = std::max(ctx->hws_max, cap);
+      ctx->mem_gen++;  // a captured forward graph must not replay old addresses
       // queued work may still read the old buffer (a host workspace is idle:
       // its previous call was waited for before this one took it)
       if (host < 0) {
@@ -99,12 +100,12 @@ struct Arena {
         cap_ = 0;
         CK(cudaMalloc(&base, cap));
       } else {
-        // stream-ordered: no device-wide synchronisation (cudaFree would
-        // stall every call in flight)
+        // stream-ordered, from the context's own pool: no device-wide
+        // synchronisation (cudaFree would stall every call in flight)
         if (base) CK(cudaFreeAsync(base, ctx->stream));
         base = nullptr;
         cap_ = 0;
-        CK(cudaMallocAsync(&base, cap, ctx->stream));
+        CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&base), cap, ctx->pool, ctx->stream));
         grew = true;
       }
       cap_ = cap;
@@ -145,6 +146,202 @@ int pack_count(sconv_cu_ctx* ctx, int in, int k, int cs, int p, int ps, int* out
   return SCONV_OK;
 }
 
+// The kernel family of one fused ECR / PECR call.  One function decides it,
+// for the launch (fused_conv) and the launch-plan query (sconv_cu_plan).
+struct KernelChoice {
+  bool smallc = false;      // ecr_smallc_kernel (C <= 4)
+  int ws = 0;               // v3 warp-specialised config id (reg_v3.inc)
+  int which = 0;            // v2 tiled config id (reg_v2.cu)
+  bool pool_after = false;  // PECR pool the epilogue does not fuse: conv, then pecr_pool_fold_kernel
+  int P = 0;                // pool extent fused into the conv epilogue (2) or 0
+  bool tiled() const { return smallc || ws || which; }
+};
+
+int choose_kernel(sconv_cu_ctx* ctx, int n, int c, int k, int kh, int kw, int stride, int OH,
+                  int OW, bool pecr, int pw, int ph, int ps, unsigned flags, KernelChoice* out) {
+  KernelChoice ch;
+  const int P = (pecr && pw == ph && pw == ps) ? pw : 0;
+  const int Pk = pecr ? (P ? P : -1) : 0;  // -1: a pool the epilogue cannot fold
+  const int forced = (flags >> 8) & 0xff;
+  const bool generic = flags & SCONV_F_GENERIC;
+  const long tiles4 = long(n) * ((OH + 3) / 4) * ((OW + 3) / 4) * ((k + 127) / 128);
+  const long tiles2 = long(n) * ((OH + 1) / 2) * ((OW + 1) / 2);
+  const bool tileable = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
+  if (forced == 'M' && !tileable)
+    return fail(ctx, SCONV_ERR_ARG, "forced kernel M does not apply to this shape");
+  if (!generic) {
+    // few input channels (VGG conv1_1): the per-warp small-C kernel (smallc.cuh)
+    ch.smallc = tileable && (forced == 'M' || (!forced && c <= 4));
+    ch.ws = ch.smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk, tiles4, tiles2);
+    ch.which = ch.ws || ch.smallc ? 0 : pick_tiled(k, kh, kw, stride, Pk);
+    // PECR with a pool the fused epilogue does not cover (anything but
+    // 2x2/2): a tiled kernel computes the conv into a workspace, then
+    // pecr_pool_fold_kernel folds the pools (the pre-pool map does reach HBM).
+    if (pecr && Pk != 2 && !ch.tiled() && !forced) {
+      ch.smallc = kh == 3 && kw == 3 && stride == 1 && k >= 32 && c <= 4;
+      ch.ws = ch.smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0, tiles4, tiles2);
+      ch.which = ch.smallc || ch.ws ? 0 : pick_tiled(k, kh, kw, stride, 0);
+      ch.pool_after = ch.tiled();
+    }
+    if (forced && forced != 'M') {
+      if (forced >= 1 && forced <= kNumCfgs) {
+        if (tileable) {
+          ch.which = forced;
+          ch.ws = 0;
+        }
+      } else if (forced >= 'A' && forced <= 'Q') {
+        if (!ws_applies(forced - 'A' + 1, k, kh, kw, stride, Pk))
+          return fail(ctx, SCONV_ERR_ARG, "forced kernel %c does not apply to this shape", forced);
+        ch.ws = forced - 'A' + 1;
+        ch.which = 0;
+      } else {
+        return fail(ctx, SCONV_ERR_ARG, "unknown forced kernel id %d", forced);
+      }
+    }
+  }
+  ch.P = ch.tiled() && !ch.pool_after ? (Pk == 2 ? 2 : 0) : 0;
+  *out = ch;
+  return SCONV_OK;
+}
+
+// CTAs one launch of `nb` images takes (chunk sizing below).
+long ctas_for(const KernelChoice& ch, int nb, int k, int OH, int OW, size_t y_img) {
+  sconv_launch_plan pl{};
+  if (ch.smallc) return long((size_t(nb) * ((OH + 3) / 4) * ((OW + 3) / 4) + 7) / 8) * ((k + 63) / 64);
+  if (ch.ws) {
+    plan_ws(&pl, ch.ws, nb, k, OH, OW);
+    return long(pl.grid_x) * pl.grid_y * pl.grid_z;
+  }
+  if (ch.which) {
+    plan_for(&pl, ch.which, nb, k, OH, OW);
+    return long(pl.grid_x) * pl.grid_y * pl.grid_z;
+  }
+  return long((size_t(nb) * y_img + 255) / 256);
+}
+
+// Image chunks (first image, images) of one call.  Host pointers: the batch
+// flows through a three-stage ring (H2D of chunk i+1, compute of chunk i, D2H
+// of chunk i-1 on three streams), so both PCIe directions stay busy.  Device
+// pointers: one chunk, unless a launch limit cuts it.
+std::vector<std::pair<int, int>> plan_chunks(const sconv_cu_ctx* ctx, const KernelChoice& ch, int n,
+                                             int k, int OH, int OW, size_t x_elems, size_t y_elems,
+                                             bool dev, bool async) {
+  static const int chunk_env = [] {  // dev override (tools/e2e_probe.py)
+    const char* e = std::getenv("SCONV_CHUNKS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const size_t y_img = y_elems / size_t(n);
+  int nchunk = 1;
+  if (!dev && n > 1) {
+    if (chunk_env > 0) {
+      nchunk = std::min(n, chunk_env);
+    } else if (async) {
+      // asynchronous calls overlap each other's transfers, so two halves
+      // (the minimum that puts H2D and D2H on their own streams) beat a finer
+      // intra-call pipeline (tools/async_probe.py: 62 ms per VGG-19 step vs
+      // 75 with the synchronous chunking, 100 with 16 chunks)
+      nchunk = 2;
+    } else {
+      // whole waves: a chunk holds the images whose CTAs fill (just under) one
+      // wave of 2 CTAs per SM, or a multiple of that when there would
+      // otherwise be more than 16 chunks (e.g. conv4_2: 28 CTAs per image ->
+      // 10-image chunks = 0.95 wave; 11 would spill 12 CTAs into a 2nd wave;
+      // tools/e2e_probe.py: conv4_2 loses 20% at 4-image chunks)
+      const double per_img = std::max(1.0, double(ctas_for(ch, n, k, OH, OW, y_img)) / n);
+      const int wave = std::max(1, static_cast<int>(2.0 * ctx->num_sms / per_img));
+      const int chunk = wave * std::max(1, (n + 16 * wave - 1) / (16 * wave));
+      nchunk = std::max(1, (n + chunk - 1) / chunk);
+    }
+  }
+  // Launch limits: the kernels index a launch's input and output with 32-bit
+  // offsets (the producer warps keep per-lane int offsets), so a launch
+  // covers at most 2^30 elements of either; the v2 tiled kernels put the
+  // images in grid.z (at most 65535).
+  const size_t lim = size_t(1) << 30;
+  const size_t big = std::max(x_elems, y_elems);
+  nchunk = std::max(nchunk, static_cast<int>(std::min<size_t>(size_t(n), (big + lim - 1) / lim)));
+  if (ch.which) nchunk = std::max(nchunk, (n + 65534) / 65535);
+  const int per = (n + nchunk - 1) / nchunk;
+  // With 4+ chunks the first and last are a quarter size, which shortens the
+  // pipeline fill (first H2D before any compute) and drain (last compute +
+  // D2H after the final H2D) of every synchronous call.
+  std::vector<std::pair<int, int>> chunks;
+  const int edge = nchunk >= 4 ? std::max(1, per / 4) : per;
+  int n0 = 0;
+  if (nchunk >= 4) {
+    chunks.push_back({0, edge});
+    n0 = edge;
+  }
+  const int tail = nchunk >= 4 ? std::min(edge, n - n0) : 0;
+  while (n0 < n - tail) {
+    const int nb = std::min(per, n - tail - n0);
+    chunks.push_back({n0, nb});
+    n0 += nb;
+  }
+  if (tail > 0) chunks.push_back({n0, tail});
+  return chunks;
+}
+
+// SCONV_F_CACHE_FILTERS: the cached slab for (pointer, shape), or nullptr.
+sconv_filter_entry* find_filters(sconv_cu_ctx* ctx, const float* src, bool host, int k, int c, int kk,
+                                 int kp) {
+  for (sconv_filter_entry& e : ctx->fcache)
+    if (e.src == src && e.host == host && e.k == k && e.c == c && e.kk == kk && e.kp == kp) return &e;
+  return nullptr;
+}
+
+void free_filter_entry(sconv_filter_entry& e) {
+  if (e.dev) cudaFree(e.dev);
+  if (e.wt) cudaFree(e.wt);
+  e.dev = e.wt = nullptr;
+}
+
+// One kernel launch over images [0, nb) of a chunk (device buffers).
+int launch_chunk(sconv_cu_ctx* ctx, const KernelChoice& ch, cudaStream_t cs, const float* dx,
+                 const float* dw, const float* wt, float* dconv, float* dy, int nb, int c, int h,
+                 int w, int k, int Kp, int kh, int kw, int stride, int OH, int OW, int pw, int ph,
+                 int ps, int mode, int PHo, int PWo, bool pecr, bool fast) {
+  const int model = ch.pool_after ? 0 : mode;
+  if (ch.smallc) {
+    SmallCArgs a{dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, model};
+    a.tiles_x = (OW + 3) / 4;
+    a.tiles_per_img = a.tiles_x * ((OH + 3) / 4);
+    a.total_tiles = a.tiles_per_img * nb;
+    const dim3 grid((a.total_tiles + 7) / 8, (k + 63) / 64);
+    if (ch.P == 2)
+      fast ? ecr_smallc_kernel<2, true><<<grid, 256, 0, cs>>>(a)
+           : ecr_smallc_kernel<2, false><<<grid, 256, 0, cs>>>(a);
+    else
+      fast ? ecr_smallc_kernel<0, true><<<grid, 256, 0, cs>>>(a)
+           : ecr_smallc_kernel<0, false><<<grid, 256, 0, cs>>>(a);
+    TRY(finish_launch(ctx, "ecr_smallc_kernel"));
+  } else if (ch.ws) {
+    WsArgs a{dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, model};
+    TRY(fast ? launch_ws_fast(ctx, ch.ws, ch.P, a) : launch_ws_exact(ctx, ch.ws, ch.P, a));
+  } else if (ch.which) {
+    TiledArgs a{dx, wt, dconv, c, h, w, k, OH, OW, 0, model};
+    TRY(launch_tiled(ctx, fast, ch.which, ch.P, a, nb));
+  } else {
+    GenericArgs a{dx, dw, dy, nb, c, h, w, k, kh, kw, stride, OH, OW, pw, ph, ps, mode, PHo, PWo};
+    const size_t y_img = pecr ? size_t(k) * PHo * PWo : size_t(k) * OH * OW;
+    const unsigned g = grid_for(size_t(nb) * y_img, 256, ctx->num_sms);
+    if (pecr) {
+      fast ? pecr_generic_kernel<true><<<g, 256, 0, cs>>>(a) : pecr_generic_kernel<false><<<g, 256, 0, cs>>>(a);
+      TRY(finish_launch(ctx, "pecr_generic_kernel"));
+    } else {
+      fast ? ecr_generic_kernel<true><<<g, 256, 0, cs>>>(a) : ecr_generic_kernel<false><<<g, 256, 0, cs>>>(a);
+      TRY(finish_launch(ctx, "ecr_generic_kernel"));
+    }
+  }
+  if (ch.pool_after) {
+    const size_t planes = size_t(nb) * k;
+    pecr_pool_fold_kernel<<<grid_for(planes * PHo * PWo, 256, ctx->num_sms), 256, 0, cs>>>(
+        dconv, dy, planes, OH, OW, pw, ph, ps, mode, PHo, PWo);
+    TRY(finish_launch(ctx, "pecr_pool_fold_kernel"));
+  }
+  return SCONV_OK;
+}
+
 // Shared body of the fused ECR / PECR entries.
 int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, const float* filt,
                int k, int kh, int kw, int stride, int pw, int ph, int ps, int mode, float* y,
@@ -170,137 +367,44 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   const bool host_async = async && !dev;
   if (n == 0 || k == 0) return SCONV_OK;
   if (!x || !filt || !y) return fail(ctx, SCONV_ERR_ARG, "null tensor pointer");
+  if (dev && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15))
+    return fail(ctx, SCONV_ERR_ARG, "device x and y must be 16-byte aligned");
+  KernelChoice ch;
+  TRY(choose_kernel(ctx, n, c, k, kh, kw, stride, OH, OW, pecr, pw, ph, ps, flags, &ch));
 
   const size_t x_elems = size_t(n) * c * h * w, w_elems = size_t(k) * c * kh * kw;
   const size_t y_elems = pecr ? size_t(n) * k * PHo * PWo : size_t(n) * k * OH * OW;
-  int P = 0;
-  if (pecr && pw == ph && pw == ps) P = pw;
-  const int Pk = pecr ? (P ? P : -1) : 0;
-  const int forced = (flags >> 8) & 0xff;
-  const long tiles4 = long(n) * ((OH + 3) / 4) * ((OW + 3) / 4) * ((k + 127) / 128);
-  const long tiles2 = long(n) * ((OH + 1) / 2) * ((OW + 1) / 2);
-  // few input channels (VGG conv1_1): the per-warp small-C kernel (smallc.cuh)
-  const bool smallc_ok = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
-  bool smallc = !(flags & SCONV_F_GENERIC) && smallc_ok &&
-                (((flags >> 8) & 0xff) == 'M' || (!((flags >> 8) & 0xff) && c <= 4));
-  int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk, tiles4, tiles2);
-  int which = (flags & SCONV_F_GENERIC) || ws || smallc ? 0 : pick_tiled(k, kh, kw, stride, Pk);
-  // PECR with a pool the fused epilogue does not cover (anything but 2x2/2):
-  // a tiled kernel computes the conv into a workspace, then
-  // pecr_pool_fold_kernel folds the pools (the pre-pool map does reach HBM).
-  bool pool_after = false;
-  if (pecr && Pk != 2 && !ws && !which && !smallc && !(flags & SCONV_F_GENERIC) &&
-      !((flags >> 8) & 0xff)) {
-    smallc = kh == 3 && kw == 3 && stride == 1 && k >= 32 && c <= 4;
-    ws = smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0, tiles4, tiles2);
-    which = smallc || ws ? 0 : pick_tiled(k, kh, kw, stride, 0);
-    pool_after = smallc || ws || which;
-  }
-  const bool tileable = kh == 3 && kw == 3 && stride == 1 && (Pk == 0 || Pk == 2) && k >= 32;
-  if (forced == 'M' && !smallc_ok)
-    return fail(ctx, SCONV_ERR_ARG, "forced kernel M does not apply to this shape");
-  if (forced && forced != 'M' && !(flags & SCONV_F_GENERIC)) {
-    if (forced >= 1 && forced <= kNumCfgs) {
-      if (tileable) {
-        which = forced;
-        ws = 0;
-      }
-    } else if (forced >= 'A' && forced <= 'Q') {
-      if (ws_applies(forced - 'A' + 1, k, kh, kw, stride, Pk)) {
-        ws = forced - 'A' + 1;
-        which = 0;
-      } else {
-        return fail(ctx, SCONV_ERR_ARG, "forced kernel %c does not apply to this shape", forced);
-      }
-    } else {
-      return fail(ctx, SCONV_ERR_ARG, "unknown forced kernel id %d", forced);
-    }
-  }
-  const int Kp = smallc ? (k + 63) / 64 * 64 : (k + 3) / 4 * 4;
+  const int Kp = ch.smallc ? (k + 63) / 64 * 64 : ch.which ? k : (k + 3) / 4 * 4;
   const bool counters = muls || adds;
+  const bool need_wt = ch.tiled();
+  const bool cache = flags & SCONV_F_CACHE_FILTERS;
 
   DeviceGuard guard(ctx->device);
-  // Host pointers: the batch is cut into image chunks that flow through a
-  // three-stage ring (up to 3 device buffers each for x and y): the H2D
-  // stream copies chunk i+1 in while the context stream computes chunk i and
-  // the D2H stream copies chunk i-1 out, so both PCIe directions stay busy
-  // (the host-pointer call is PCIe-bound: 2.9 GB in / 2.6 GB out per VGG-19
-  // step against ~29 ms of kernels).  Events order the reuse of every ring
-  // slot.  Device pointers: one chunk on the context stream.
-  static const int chunk_env = [] {  // dev override (tools/e2e_probe.py)
-    const char* e = std::getenv("SCONV_CHUNKS");
-    return e ? std::atoi(e) : 0;
-  }();
-  // Chunk size: small enough to keep both PCIe directions busy, large enough
-  // that one chunk's launch still fills about one wave of CTAs (measured,
-  // tools/e2e_probe.py: conv4_2 loses 20% at 4-image chunks).
-  auto ctas_for = [&](int nb) -> long {
-    sconv_launch_plan pl{};
-    if (smallc) return long((size_t(nb) * ((OH + 3) / 4) * ((OW + 3) / 4) + 7) / 8) * ((k + 63) / 64);
-    if (ws) {
-      plan_ws(&pl, ws, nb, k, OH, OW);
-      return long(pl.grid_x) * pl.grid_y * pl.grid_z;
-    }
-    if (which) {
-      plan_for(&pl, which, nb, k, OH, OW);
-      return long(pl.grid_x) * pl.grid_y * pl.grid_z;
-    }
-    return long((size_t(nb) * y_elems / std::max(n, 1) + 255) / 256);
-  };
-  int nchunk = 1;
-  if (!dev && n > 1) {
-    if (chunk_env > 0) {
-      nchunk = std::min(n, chunk_env);
-    } else if (async) {
-      // asynchronous calls overlap each other's transfers, so two halves
-      // (the minimum that puts H2D and D2H on their own streams) beat a finer
-      // intra-call pipeline (tools/async_probe.py: 62 ms per VGG-19 step vs
-      // 75 with the synchronous chunking, 100 with 16 chunks)
-      nchunk = 2;
-    } else {
-      // whole waves: a chunk holds the images whose CTAs fill (just under) one
-      // wave of 2 CTAs per SM, or a multiple of that when there would
-      // otherwise be more than 16 chunks (e.g. conv4_2: 28 CTAs per image ->
-      // 10-image chunks = 0.95 wave; 11 would spill 12 CTAs into a 2nd wave)
-      const double per_img = std::max(1.0, double(ctas_for(n)) / n);
-      const int wave = std::max(1, static_cast<int>(2.0 * ctx->num_sms / per_img));
-      const int chunk = wave * std::max(1, (n + 16 * wave - 1) / (16 * wave));
-      nchunk = std::max(1, (n + chunk - 1) / chunk);
-    }
-  }
-  // The kernels index a launch's input and output with 32-bit offsets (the
-  // producer warps keep per-lane int offsets): a launch covers at most 2^30
-  // elements of either, so larger batches are cut into image chunks.
-  {
-    const size_t lim = size_t(1) << 30;
-    const size_t big = std::max(x_elems, y_elems);
-    const int need = static_cast<int>(std::min<size_t>(size_t(n), (big + lim - 1) / lim));
-    nchunk = std::max(nchunk, need);
-  }
-  const int per = (n + nchunk - 1) / nchunk;
-  // Chunk list: with 4+ chunks the first and last are a quarter size, which
-  // shortens the pipeline fill (first H2D before any compute) and drain (last
-  // compute + D2H after the final H2D) of every synchronous call.
-  std::vector<std::pair<int, int>> chunks;  // (first image, images)
-  {
-    const int edge = nchunk >= 4 ? std::max(1, per / 4) : per;
-    int n0 = 0;
-    if (nchunk >= 4) {
-      chunks.push_back({0, edge});
-      n0 = edge;
-    }
-    const int tail = nchunk >= 4 ? std::min(edge, n - n0) : 0;
-    while (n0 < n - tail) {
-      const int nb = std::min(per, n - tail - n0);
-      chunks.push_back({n0, nb});
-      n0 += nb;
-    }
-    if (tail > 0) chunks.push_back({n0, tail});
-  }
-  nchunk = static_cast<int>(chunks.size());
+  const std::vector<std::pair<int, int>> chunks =
+      plan_chunks(ctx, ch, n, k, OH, OW, x_elems, y_elems, dev, async);
+  const int nchunk = static_cast<int>(chunks.size());
+  int per = 0;
+  for (const auto& cp : chunks) per = std::max(per, cp.second);
   const size_t x_img = size_t(c) * h * w, y_img = y_elems / size_t(n);
   const int nbuf = dev ? 0 : std::min(nchunk, 3);
   const bool piped = !dev && nchunk > 1;
+
+  // Filters for SCONV_F_CACHE_FILTERS: the context's copy, made on first use.
+  sconv_filter_entry* fe = cache ? find_filters(ctx, filt, !dev, k, c, kh * kw, need_wt ? Kp : 0) : nullptr;
+  const bool fresh = cache && !fe;
+  if (fresh) {
+    if (ctx->fcache.size() >= 64) {  // bounded: drop the oldest entry
+      CK(cudaDeviceSynchronize());
+      free_filter_entry(ctx->fcache.front());
+      ctx->fcache.erase(ctx->fcache.begin());
+    }
+    sconv_filter_entry e{filt, !dev, k, c, kh * kw, need_wt ? Kp : 0, nullptr, nullptr};
+    if (!dev) CK(cudaMalloc(&e.dev, w_elems * 4));
+    if (need_wt) CK(cudaMalloc(&e.wt, size_t(Kp) * c * kh * kw * 4));
+    ctx->fcache.push_back(e);
+    fe = &ctx->fcache.back();
+  }
+
   Arena ar{ctx, {}};
   if (host_async) {  // take the next host workspace once its previous call is done
     ar.host = ctx->hws_next;
@@ -313,17 +417,16 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     i_x[b] = ar.add(size_t(per) * x_img * 4);
     i_y[b] = ar.add(size_t(per) * y_img * 4);
   }
-  const size_t i_w = dev ? 0 : ar.add(w_elems * 4);
-  const size_t i_wt = (which || ws || smallc) ? ar.add(size_t(Kp) * c * kh * kw * 4) : 0;
+  const size_t i_w = dev || fe ? 0 : ar.add(w_elems * 4);
+  const size_t i_wt = need_wt && !fe ? ar.add(size_t(Kp) * c * kh * kw * 4) : 0;
   for (int b = 0; b < (counters ? std::max(nbuf, 1) : 0); ++b) i_pix[b] = ar.add(size_t(per) * h * w * 4);
-  const size_t conv_img = size_t(k) * OH * OW;
-  const size_t i_conv = pool_after ? ar.add(size_t(per) * conv_img * 4) : 0;
+  const size_t i_conv = ch.pool_after ? ar.add(size_t(per) * k * OH * OW * 4) : 0;
   const size_t i_ops = ar.add(64);
   std::vector<char*> p;
   TRY(ar.commit(p));
-  const float* dw = dev ? filt : reinterpret_cast<float*>(p[i_w]);
+  const float* dw = dev ? filt : fe ? fe->dev : reinterpret_cast<float*>(p[i_w]);
   auto* dops = reinterpret_cast<unsigned long long*>(p[i_ops]);
-  float* wt = (which || ws || smallc) ? reinterpret_cast<float*>(p[i_wt]) : nullptr;
+  const float* wt = !need_wt ? nullptr : fe ? fe->wt : reinterpret_cast<float*>(p[i_wt]);
   cudaStream_t st = ctx->stream;
   if (piped && !ctx->h2d) {
     CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
@@ -341,27 +444,23 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_done, 0));
     CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_done, 0));
   }
-  // filters: copy (host path), re-layout for the tiled kernels, once per call.
-  // Async host calls send them on the H2D stream, ahead of this call's input
-  // chunks: issued on the context stream they would queue behind every input
-  // copy already submitted to the H2D engine (the previous calls' inputs).
-  if (!dev) {
+  // Filters: copy (host path) and re-layout for the tiled kernels, once per
+  // call -- or once per cached slab.  Async host calls send them on the H2D
+  // stream, ahead of this call's input chunks: issued on the context stream
+  // they would queue behind every input copy already submitted to the H2D
+  // engine (the previous calls' inputs).
+  if (!dev && (!fe || fresh)) {
     if (host_async && piped) {
-      CK(cudaMemcpyAsync(const_cast<float*>(dw), filt, w_elems * 4, cudaMemcpyHostToDevice,
-                         ctx->h2d));
+      CK(cudaMemcpyAsync(const_cast<float*>(dw), filt, w_elems * 4, cudaMemcpyHostToDevice, ctx->h2d));
       CK(cudaEventRecord(ctx->ev_done, ctx->h2d));
       CK(cudaStreamWaitEvent(st, ctx->ev_done, 0));
     } else {
       CK(cudaMemcpyAsync(const_cast<float*>(dw), filt, w_elems * 4, cudaMemcpyHostToDevice, st));
     }
   }
-  if (ws || smallc) {
+  if (need_wt && (!fe || fresh)) {
     transpose_filters_kernel<<<grid_for(size_t(Kp) * c * kh * kw, 256, ctx->num_sms), 256, 0, st>>>(
-        dw, wt, k, Kp, c, kh * kw);
-    TRY(finish_launch(ctx, "transpose_filters_kernel"));
-  } else if (which) {
-    transpose_filters_kernel<<<grid_for(w_elems, 256, ctx->num_sms), 256, 0, st>>>(dw, wt, k, k, c,
-                                                                                    kh * kw);
+        dw, const_cast<float*>(wt), k, Kp, c, kh * kw);
     TRY(finish_launch(ctx, "transpose_filters_kernel"));
   }
   if (counters) CK(cudaMemsetAsync(dops, 0, 16, st));
@@ -380,9 +479,7 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     cudaStream_t cs = st;
     const float* dx = dev ? x + size_t(n0) * x_img : reinterpret_cast<float*>(p[i_x[b]]);
     float* dy = dev ? y + size_t(n0) * y_img : reinterpret_cast<float*>(p[i_y[b]]);
-    float* dconv = pool_after ? reinterpret_cast<float*>(p[i_conv]) : dy;  // conv kernels write here
-    const int Pl = pool_after ? 0 : P;
-    const int model = pool_after ? 0 : mode;
+    float* dconv = ch.pool_after ? reinterpret_cast<float*>(p[i_conv]) : dy;  // conv kernels write here
     if (!dev) {
       cudaStream_t hs = piped ? ctx->h2d : st;
       if (piped && ci >= nbuf) CK(cudaStreamWaitEvent(hs, ctx->ev_comp[b], 0));  // x slot free
@@ -394,48 +491,8 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
         if (ci >= nbuf) CK(cudaStreamWaitEvent(cs, ctx->ev_out[b], 0));  // y slot drained
       }
     }
-    if (smallc) {
-      SmallCArgs a{dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, model};
-      a.tiles_x = (OW + 3) / 4;
-      a.tiles_per_img = a.tiles_x * ((OH + 3) / 4);
-      a.total_tiles = a.tiles_per_img * nb;
-      const dim3 grid((a.total_tiles + 7) / 8, (k + 63) / 64);
-      if (Pl == 2)
-        fast ? ecr_smallc_kernel<2, true><<<grid, 256, 0, cs>>>(a)
-             : ecr_smallc_kernel<2, false><<<grid, 256, 0, cs>>>(a);
-      else
-        fast ? ecr_smallc_kernel<0, true><<<grid, 256, 0, cs>>>(a)
-             : ecr_smallc_kernel<0, false><<<grid, 256, 0, cs>>>(a);
-      TRY(finish_launch(ctx, "ecr_smallc_kernel"));
-    } else if (ws) {
-      WsArgs a{dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, model};
-      TRY(fast ? launch_ws_fast(ctx, ws, Pl, a) : launch_ws_exact(ctx, ws, Pl, a));
-    } else if (which) {
-      TiledArgs a{dx, wt, dconv, c, h, w, k, OH, OW, 0, model};
-      TRY(launch_tiled(ctx, fast, which, Pl, a, nb));
-    } else {
-      GenericArgs a{dx, dw, dy, nb, c, h, w, k, kh, kw, stride, OH, OW, pw, ph, ps, mode, PHo, PWo};
-      const unsigned g = grid_for(size_t(nb) * y_img, 256, ctx->num_sms);
-      if (pecr) {
-        if (fast)
-          pecr_generic_kernel<true><<<g, 256, 0, cs>>>(a);
-        else
-          pecr_generic_kernel<false><<<g, 256, 0, cs>>>(a);
-        TRY(finish_launch(ctx, "pecr_generic_kernel"));
-      } else {
-        if (fast)
-          ecr_generic_kernel<true><<<g, 256, 0, cs>>>(a);
-        else
-          ecr_generic_kernel<false><<<g, 256, 0, cs>>>(a);
-        TRY(finish_launch(ctx, "ecr_generic_kernel"));
-      }
-    }
-    if (pool_after) {
-      const size_t planes = size_t(nb) * k;
-      pecr_pool_fold_kernel<<<grid_for(planes * PHo * PWo, 256, ctx->num_sms), 256, 0, cs>>>(
-          dconv, dy, planes, OH, OW, pw, ph, ps, mode, PHo, PWo);
-      TRY(finish_launch(ctx, "pecr_pool_fold_kernel"));
-    }
+    TRY(launch_chunk(ctx, ch, cs, dx, dw, wt, dconv, dy, nb, c, h, w, k, Kp, kh, kw, stride, OH, OW,
+                     pw, ph, ps, mode, PHo, PWo, pecr, fast));
     if (counters) {  // integer atomics: order-free across chunks
       int32_t* pix = reinterpret_cast<int32_t*>(p[i_pix[b]]);
       pixel_nnz_kernel<<<grid_for(size_t(nb) * h * w, 256, ctx->num_sms), 256, 0, cs>>>(dx, nb, c, h,
@@ -561,13 +618,21 @@ int sconv_cu_ctx_create(int device, sconv_cu_ctx** out) {
   ctx = new sconv_cu_ctx();
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
-  {  // async host-call workspaces come from the device's default memory pool:
-     // keep freed blocks mapped instead of trimming them at every sync point
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  {  // async host-call workspaces come from the context's own memory pool,
+     // which keeps freed blocks mapped instead of trimming them at every sync
+     // point (the device's default pool, which the application may use, is
+     // left alone)
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    e = cudaMemPoolCreate(&ctx->pool, &props);
+    if (e != cudaSuccess) {
+      delete ctx;
+      return fail(nullptr, SCONV_ERR_CUDA, "cudaMemPoolCreate: %s", cudaGetErrorString(e));
     }
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
   ctx->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
   DeviceGuard guard(device);
@@ -597,6 +662,9 @@ int sconv_cu_ctx_destroy(sconv_cu_ctx* ctx) {
       if (ctx->ev_hws[a]) cudaEventDestroy(ctx->ev_hws[a]);
     }
     cudaStreamSynchronize(ctx->stream);
+    for (sconv_filter_entry& fe : ctx->fcache) free_filter_entry(fe);
+    ctx->fcache.clear();
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     if (ctx->fwd) cudaFree(ctx->fwd);
     if (ctx->fwd_graph) cudaGraphExecDestroy(ctx->fwd_graph);
     if (ctx->ev_graph) cudaEventDestroy(ctx->ev_graph);
@@ -648,6 +716,16 @@ const char* sconv_cu_last_error(const sconv_cu_ctx* ctx) {
 
 uint64_t sconv_cu_launch_count(const sconv_cu_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int sconv_cu_release_filters(sconv_cu_ctx* ctx) {
+  if (!ctx) return SCONV_ERR_ARG;
+  DeviceGuard guard(ctx->device);
+  CK(cudaDeviceSynchronize());  // cached slabs may be read by work in flight
+  for (sconv_filter_entry& fe : ctx->fcache) free_filter_entry(fe);
+  ctx->fcache.clear();
+  ctx->tmaps.clear();
+  return SCONV_OK;
+}
+
 int sconv_conv_output_dims(int in_w, int in_h, int k_w, int k_h, int stride, int* out_w,
                            int* out_h) {
   if (!out_w || !out_h) return SCONV_ERR_ARG;
@@ -667,25 +745,16 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
   if (c < 1) return fail(nullptr, SCONV_ERR_SHAPE, "channels must be positive");
   int OW, OH;
   TRY(conv_dims(nullptr, w, h, kw, kh, stride, &OW, &OH));
-  int P = 0, PWo = OW, PHo = OH;
+  int PWo = OW, PHo = OH;
   if (pool_w > 0) {
     TRY(pack_count(nullptr, w, kw, stride, pool_w, pool_stride, &PWo));
     TRY(pack_count(nullptr, h, kh, stride, pool_h, pool_stride, &PHo));
-    P = (pool_w == pool_h && pool_w == pool_stride) ? pool_w : -1;
   }
-  const int forced = (flags >> 8) & 0xff;
-  const long tiles4 = long(n) * ((OH + 3) / 4) * ((OW + 3) / 4) * ((k + 127) / 128);
-  const long tiles2 = long(n) * ((OH + 1) / 2) * ((OW + 1) / 2);
-  bool smallc = !(flags & SCONV_F_GENERIC) && kh == 3 && kw == 3 && stride == 1 &&
-                (P == 0 || P == 2) && k >= 32 && (forced == 'M' || (!forced && c <= 4));
-  int ws = (flags & SCONV_F_GENERIC) || smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, P, tiles4, tiles2);
-  int which = (flags & SCONV_F_GENERIC) || ws || smallc ? 0 : pick_tiled(k, kh, kw, stride, P);
-  if (pool_w > 0 && P != 2 && !ws && !which && !smallc && !(flags & SCONV_F_GENERIC) && !forced) {
-    // conv by a tiled kernel, then pecr_pool_fold_kernel (see fused_conv)
-    smallc = kh == 3 && kw == 3 && stride == 1 && k >= 32 && c <= 4;
-    ws = smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0, tiles4, tiles2);
-    which = smallc || ws ? 0 : pick_tiled(k, kh, kw, stride, 0);
-  }
+  KernelChoice ch;
+  TRY(choose_kernel(nullptr, n, c, k, kh, kw, stride, OH, OW, pool_w > 0, pool_w, pool_h,
+                    pool_stride, flags, &ch));
+  const bool smallc = ch.smallc;
+  const int ws = ch.ws, which = ch.which;
   if (smallc) {
     const long tiles = long(n) * ((OH + 3) / 4) * ((OW + 3) / 4);
     out->kernel = 300;
@@ -783,6 +852,10 @@ int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int
     if (!layers[l].filters) return fail(ctx, SCONV_ERR_ARG, "layer %d: null filters", l);
   const bool dev = flags & SCONV_F_DEVICE;
   const bool counters = muls || adds;
+  if ((flags & SCONV_F_GRAPH) && (!dev || counters))
+    return fail(ctx, SCONV_ERR_ARG, "SCONV_F_GRAPH needs device pointers and no counters");
+  if (dev && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15))
+    return fail(ctx, SCONV_ERR_ARG, "device x and y must be 16-byte aligned");
 
   // device residency: input, every layer's filters (host pointers only),
   // two activation buffers and one pre-pool conv buffer
@@ -804,6 +877,7 @@ int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int
     if (ctx->fwd) CK(cudaFree(ctx->fwd));
     ctx->fwd = nullptr;
     ctx->fwd_cap = 0;
+    ctx->mem_gen++;
     CK(cudaMalloc(&ctx->fwd, need));
     ctx->fwd_cap = need;
   }
@@ -829,8 +903,6 @@ int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int
     CK(cudaMemcpyAsync(buf[0], x, size_t(n) * c * h * w * 4, cudaMemcpyHostToDevice, st));
     cur0 = buf[0];
   }
-  if ((flags & SCONV_F_GRAPH) && (!dev || counters))
-    return fail(ctx, SCONV_ERR_ARG, "SCONV_F_GRAPH needs device pointers and no counters");
   const unsigned kflags = (flags & (SCONV_F_FAST | SCONV_F_GENERIC | (0xffu << 8))) | SCONV_F_DEVICE |
                           (counters ? 0u : SCONV_F_ASYNC);
   const cudaMemcpyKind out_kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -911,7 +983,9 @@ int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int
       add(o, sizeof o);
     }
     add(&flags, sizeof flags);
-    if (ctx->fwd_graph && ctx->fwd_key == key) {
+    // a graph captured before any workspace it points into was reallocated
+    // (a larger call on this context since) is stale: re-capture
+    if (ctx->fwd_graph && ctx->fwd_key == key && ctx->fwd_gen == ctx->mem_gen) {
       CK(cudaEventRecord(ctx->ev_graph, st));
       CK(cudaStreamWaitEvent(ctx->own, ctx->ev_graph, 0));
       CK(cudaGraphLaunch(ctx->fwd_graph, ctx->own));
@@ -950,6 +1024,7 @@ int sconv_cu_forward(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int
       if (ei != cudaSuccess) return fail(ctx, SCONV_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ei));
       ctx->fwd_graph = exec;
       ctx->fwd_key = key;
+      ctx->fwd_gen = ctx->mem_gen;
     }
   }
   CK(cudaStreamSynchronize(st));
