@@ -282,6 +282,48 @@ int sconv_cu_pecr_conv_pool_multi(sconv_cu_ctx** ctxs, int nctx,
                                   uint64_t* muls, uint64_t* adds,
                                   unsigned flags);
 
+/* ---- compressed ingest ---------------------------------------------------
+ * A batch of n maps [C][H][W] can cross PCIe as its nonzero bitmap plus the
+ * packed nonzeros instead of dense fp32 (the transfer saving the paper
+ * credits its compressed formats with); the GPU expands it in
+ * HBM right before the convolution.  Per image, E = C*H*W elements:
+ *   bits   [n][words]       words = ceil(E / 32); bit e % 32 of word e / 32
+ *                           set iff element e is nonzero (v != 0.0f: -0 is a
+ *                           zero, as in ecr_convert, src/ecr.cpp:84)
+ *   base   [n][blocks + 1]  blocks = ceil(words / 32) (1024 elements each):
+ *                           offset in `values` of the block's first nonzero;
+ *                           base[i][blocks] = one past image i's last one
+ *   values [nnz]            every image's nonzeros in element order
+ * Offsets are absolute, so image i's nonzeros start at base[i][0].  With host
+ * pointers the calls copy exactly these bytes; with SCONV_F_DEVICE they read
+ * them from device memory. */
+int sconv_packed_dims(int c, int h, int w, int64_t* words, int64_t* blocks);
+/* Pack dense maps (host, `threads` threads, 0 = all cores).  With bits,
+ * base and values all NULL only *nnz is computed (size query); otherwise
+ * values must hold `capacity` >= nnz floats. */
+int sconv_pack_maps(const float* x, int n, int c, int h, int w, uint32_t* bits,
+                    int64_t* base, float* values, int64_t capacity,
+                    int64_t* nnz, int threads);
+/* sconv_cu_ecr_conv / sconv_cu_pecr_conv_pool on a packed batch; outputs,
+ * flags and results are those of the dense entries (bit-identical). */
+int sconv_cu_ecr_conv_packed(sconv_cu_ctx* ctx, const uint32_t* bits,
+                             const int64_t* base, const float* values, int n,
+                             int c, int h, int w, const float* filters, int k,
+                             int kh, int kw, int stride, float* y,
+                             uint64_t* muls, uint64_t* adds, unsigned flags);
+int sconv_cu_pecr_conv_pool_packed(sconv_cu_ctx* ctx, const uint32_t* bits,
+                                   const int64_t* base, const float* values,
+                                   int n, int c, int h, int w,
+                                   const float* filters, int k, int kh, int kw,
+                                   int stride, int pool_w, int pool_h,
+                                   int pool_stride, int mode, float* y,
+                                   uint64_t* muls, uint64_t* adds,
+                                   unsigned flags);
+/* Expand a packed batch into dense x [n][C][H][W] (device pointers only). */
+int sconv_cu_unpack_maps(sconv_cu_ctx* ctx, const uint32_t* bits,
+                         const int64_t* base, const float* values, int n, int c,
+                         int h, int w, float* x, unsigned flags);
+
 /* ---- synthetic inputs (host) ------------------------------------------- */
 /* Bit-identical to sconv::generate (src/dataset.cpp:77-100): xoshiro256**
  * seeded by SplitMix64, floor(s*N) zeros at Fisher-Yates positions, nonzeros

@@ -14,7 +14,8 @@ from .api import (ConvConfig, EcrBlockRow, EcrDims, EcrGridShape, EcrMap, ExecCo
                   Method, LayerSpec, NetworkSpec, ForwardResult, TrafficReport, forward,
                   forward_batched, load, save, load_batch, synchronize,
                   SparsityProfile, window_nnz_counts, sparsity_profile,
-                  ecr_conv_multi, pecr_conv_pool_multi)
+                  ecr_conv_multi, pecr_conv_pool_multi,
+                  PackedMaps, pack_maps, unpack_maps)
 from ._native import LIB_PATH, SYMBOLS, Context, context
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -27,7 +27,8 @@ SYMBOLS = (
     "sconv_cu_pecr_conv_pool_multi", "sconv_generate", "sconv_generate_batch", "sconv_checksum",
     "sconv_cu_forward", "sconv_cu_forward_dims", "sconv_io_last_error", "sconv_map_file_dims",
     "sconv_load_map", "sconv_save_map", "sconv_load_maps", "sconv_cu_window_nnz",
-    "sconv_cu_release_filters",
+    "sconv_cu_release_filters", "sconv_packed_dims", "sconv_pack_maps", "sconv_cu_ecr_conv_packed",
+    "sconv_cu_pecr_conv_pool_packed", "sconv_cu_unpack_maps",
 )
 
 F_EXACT = 0
@@ -92,6 +93,14 @@ def lib() -> C.CDLL:
     L.sconv_cu_launch_count.argtypes = [_vp]
     L.sconv_cu_launch_count.restype = C.c_uint64
     L.sconv_cu_release_filters.argtypes = [_vp]
+    _i64p = C.POINTER(C.c_int64)
+    L.sconv_packed_dims.argtypes = [_i, _i, _i, _i64p, _i64p]
+    L.sconv_pack_maps.argtypes = [_vp, _i, _i, _i, _i, _vp, _vp, _vp, C.c_int64, _i64p, _i]
+    L.sconv_cu_ecr_conv_packed.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 4 + [_vp] + [_i] * 4 + [
+        _vp, _u64p, _u64p, C.c_uint]
+    L.sconv_cu_pecr_conv_pool_packed.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 4 + [_vp] + [
+        _i] * 8 + [_vp, _u64p, _u64p, C.c_uint]
+    L.sconv_cu_unpack_maps.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 4 + [_vp, C.c_uint]
     L.sconv_conv_output_dims.argtypes = [_i] * 5 + [C.POINTER(_i)] * 2
     L.sconv_pecr_pack_count.argtypes = [_i] * 5 + [C.POINTER(_i)]
     L.sconv_cu_plan.argtypes = [_i] * 11 + [C.c_uint, C.POINTER(LaunchPlan)]

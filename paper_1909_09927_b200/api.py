@@ -478,6 +478,124 @@ def _aligned16(t):
     return t if t.data_ptr() % 16 == 0 else t.clone()
 
 
+@dataclass
+class PackedMaps:
+    """A batch [n, C, H, W] in the compressed-ingest layout (include/sconv_cuda.h):
+    nonzero bitmap `bits` [n, words] (uint32), block offsets `base`
+    [n, blocks + 1] (int64, absolute into `values`) and the packed nonzeros
+    `values` (float32).  numpy arrays (host; the entries copy exactly these
+    bytes) or CUDA tensors (device, see `to`)."""
+    shape: tuple
+    bits: object
+    base: object
+    values: object
+
+    @property
+    def nbytes(self) -> int:
+        """Bytes that cross PCIe for this batch."""
+        return int(sum(_nbytes(a) for a in (self.bits, self.base, self.values)))
+
+    def to(self, device) -> "PackedMaps":
+        import torch
+        t = lambda a: (a if _is_torch_cuda(a) else torch.from_numpy(np.asarray(a))).to(device)
+        return PackedMaps(self.shape, t(self.bits), t(self.base), t(self.values))
+
+
+def _nbytes(a) -> int:
+    return a.nbytes if isinstance(a, np.ndarray) else a.numel() * a.element_size()
+
+
+def pack_maps(x, threads: int = 0) -> PackedMaps:
+    """Dense maps [n, C, H, W] (numpy) -> PackedMaps (host, sconv_pack_maps)."""
+    x = np.ascontiguousarray(x, np.float32)
+    if x.ndim != 4:
+        raise ShapeError("pack_maps takes [n, C, H, W]")
+    n, c, h, w = x.shape
+    L = nat.lib()
+    words, blocks = C.c_int64(), C.c_int64()
+    nat.check(L.sconv_packed_dims(c, h, w, C.byref(words), C.byref(blocks)))
+    nnz = C.c_int64()
+    nat.check(L.sconv_pack_maps(_ptr(x), n, c, h, w, None, None, None, 0, C.byref(nnz), threads))
+    bits = np.empty((n, words.value), np.uint32)
+    base = np.empty((n, blocks.value + 1), np.int64)
+    values = np.empty(max(nnz.value, 1), np.float32)
+    nat.check(L.sconv_pack_maps(_ptr(x), n, c, h, w, _ptr(bits), _ptr(base), _ptr(values),
+                                values.size, C.byref(nnz), threads))
+    return PackedMaps((n, c, h, w), bits, base, values[:nnz.value])
+
+
+def unpack_maps(p: PackedMaps):
+    """Expand a device-resident PackedMaps into a dense CUDA tensor
+    (sconv_cu_unpack_maps, the kernel the packed entries run before the conv)."""
+    import torch
+    if not _is_torch_cuda(p.bits):
+        raise ShapeError("unpack_maps takes a device PackedMaps (PackedMaps.to)")
+    out = torch.empty(p.shape, dtype=torch.float32, device=p.bits.device)
+    ctx = nat.context(p.bits.device.index)
+    ctx.set_stream(torch.cuda.current_stream(p.bits.device).cuda_stream)
+    nat.check(nat.lib().sconv_cu_unpack_maps(ctx.handle, p.bits.data_ptr(), p.base.data_ptr(),
+                                             p.values.data_ptr(), *p.shape, out.data_ptr(),
+                                             nat.F_DEVICE), ctx.handle)
+    return out
+
+
+def _batched_packed(kind: str, p: PackedMaps, filters, stride: int, pool, mode: int, fast: bool,
+                    counters, device: Optional[int], out, sync: bool, flags: int):
+    L = nat.lib()
+    N, Cc, H, W = p.shape
+    dev_in = _is_torch_cuda(p.bits)
+    if dev_in:
+        import torch
+        filters = filters.contiguous()
+        dev = p.bits.device.index if device is None else device
+        ctx = nat.context(dev)
+        ctx.set_stream(torch.cuda.current_stream(p.bits.device).cuda_stream)
+        flags |= nat.F_DEVICE
+        if not sync and counters is None:
+            flags |= nat.F_ASYNC
+        ptr = lambda a: a.data_ptr()
+    else:
+        filters = np.ascontiguousarray(filters, np.float32)
+        ctx = nat.context(0 if device is None else device)
+        ctx.use_own_stream()
+        ptr = _ptr
+    K, Cf, kh, kw = filters.shape
+    if Cf != Cc:
+        raise ShapeError(f"filter channels {Cf} != map channels {Cc}")
+    if kind == "ecr":
+        od = conv_output_dims(W, H, kw, kh, stride)
+        shape = (N, K, od.height, od.width)
+    else:
+        shape = (N, K, pecr_pack_count(H, kh, stride, pool[1], pool[2]),
+                 pecr_pack_count(W, kw, stride, pool[0], pool[2]))
+    if out is None:
+        if dev_in:
+            import torch
+            out = torch.empty(shape, dtype=torch.float32, device=p.bits.device)
+        else:
+            out = np.empty(shape, np.float32)
+    elif tuple(out.shape) != shape:
+        raise ShapeError("out has the wrong shape")
+    if not dev_in and not sync and counters is None:
+        flags |= nat.F_ASYNC
+        ctx.keep(p.bits, p.base, p.values, filters, out)
+    m, a = C.c_uint64(0), C.c_uint64(0)
+    mp = C.byref(m) if counters is not None else None
+    ap = C.byref(a) if counters is not None else None
+    vp = ptr(p.values) if _nbytes(p.values) else None
+    if kind == "ecr":
+        st = L.sconv_cu_ecr_conv_packed(ctx.handle, ptr(p.bits), ptr(p.base), vp, N, Cc, H, W,
+                                        ptr(filters), K, kh, kw, stride, ptr(out), mp, ap, flags)
+    else:
+        st = L.sconv_cu_pecr_conv_pool_packed(ctx.handle, ptr(p.bits), ptr(p.base), vp, N, Cc, H,
+                                              W, ptr(filters), K, kh, kw, stride, pool[0],
+                                              pool[1], pool[2], int(mode), ptr(out), mp, ap, flags)
+    nat.check(st, ctx.handle)
+    if counters is not None:
+        counters.merge(OpCount(m.value, a.value))
+    return out
+
+
 def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, counters,
              device: Optional[int], generic: bool, out, sync: bool, kernel=0,
              cache_filters: bool = False):
@@ -487,6 +605,9 @@ def _batched(kind: str, x, filters, stride: int, pool, mode: int, fast: bool, co
         flags |= nat.F_CACHE_FILTERS
     if kernel:
         flags |= nat.F_KERNEL(kernel)
+    if isinstance(x, PackedMaps):  # compressed ingest
+        return _batched_packed(kind, x, filters, stride, pool, mode, fast, counters, device, out,
+                               sync, flags)
     if _is_torch_cuda(x):
         import torch
         if not (_is_torch_cuda(filters) and x.dtype == torch.float32 and filters.dtype == torch.float32):

@@ -108,7 +108,9 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4 = 1L
 bool ws_applies(int id, int K, int kh, int kw, int S, int P);  // forced-config shape check
 int launch_ws_fast(sconv_cu_ctx* ctx, int which, int P, const WsArgs& a);
 int launch_ws_exact(sconv_cu_ctx* ctx, int which, int P, const WsArgs& a);
-void plan_ws(sconv_launch_plan* p, int which, int N, int K, int OH, int OW);
+void plan_ws(sconv_launch_plan* p, int which, int N, int K, int OH, int OW, int pw = 0, int ph = 0,
+             int ps = 1);
+int pick_ws_pool(int K, int kh, int kw, int S, int pw, int ph);  // general-pool config, 0 = none
 
 }  // namespace host
 }  // namespace sconv_cu

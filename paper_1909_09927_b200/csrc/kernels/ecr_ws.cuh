@@ -34,6 +34,10 @@
 
 namespace sconv_cu {
 
+#ifndef SCONV_EMPTY_ALL_LANES  // 1: every consumer lane arrives on `empty` (sanitizer build)
+#define SCONV_EMPTY_ALL_LANES 0
+#endif
+
 #ifndef SCONV_SPARSE_PCT_WIDE  // see WsCfg::SPARSE_PCT
 #define SCONV_SPARSE_PCT_WIDE 25
 #endif
@@ -55,7 +59,11 @@ struct WsCfg {
   static constexpr int NT = 32 * (WPC + 1);          // + producer warp
   static constexpr int MINB =  // CTAs/SM (register budget: accumulators + weight registers)
       (NT > 256 || R >= 8) ? 1 : ((TH * TW * R <= 32 && KH * KW * R <= 36) ? 3 : 2);
-  static constexpr int SMEM_BYTES = NS * STAGE * 4 + 2 * NS * 8;
+  // P == -1 (any pool geometry): the epilogue stages each warp's conv tile in
+  // shared memory, aliased onto the ring once every consumer has left it
+  static constexpr int EPI = P < 0 ? WPC * TH * TW * KT : 0;
+  static constexpr int RING = NS * STAGE > EPI ? NS * STAGE : EPI;  // floats before the barriers
+  static constexpr int SMEM_BYTES = RING * 4 + 2 * NS * 8;
   static constexpr int CELLS = WPC * NPOS;           // input cells per channel
   static constexpr int CELLS_PER_LANE = (CELLS + 31) / 32;
   // Producer copies cells in 8-byte pairs when every window row starts on an
@@ -81,7 +89,7 @@ struct WsCfg {
   static constexpr int PAIRS_PER_LANE = (PAIRS + 31) / 32;
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
   static_assert(R == 2 || R == 4 || R == 8, "R");
-  static_assert(P == 0 || (TH % P == 0 && TW % P == 0), "pool tile");
+  static_assert(P <= 0 || (TH % P == 0 && TW % P == 0), "pool tile");
   static_assert((IN_STAGE * 4) % 128 == 0 && (STAGE * 4) % 128 == 0, "TMA destination alignment");
   static constexpr unsigned W_BYTES = W_STAGE * 4;   // one TMA box (CC x KK x KT floats)
 };
@@ -89,10 +97,16 @@ struct WsCfg {
 struct WsArgs {
   const float* x;   // [N][C][H][W]
   const float* wt;  // [C][KH*KW][Kp]  (filters transposed once per call)
-  float* y;         // [N][K][OH][OW] or pooled [N][K][OH/P][OW/P]
+  float* y;         // [N][K][OH][OW] or pooled [N][K][PHo][PWo]
   int N, C, H, W, K, Kp, OH, OW;
   int tiles_x, tiles_per_img, total_tiles;
-  int mode;  // pool mode (P > 0)
+  int mode;  // pool mode (P != 0); P == 0: fused ReLU flag
+  // P == -1: the pool window / stride and the pooled map; a warp tile then
+  // holds PTH x PTW whole pool windows ((PTH-1)*ps + ph <= TH conv rows) and
+  // consecutive tiles start tsy / tsx conv outputs apart (= PTH*ps, PTW*ps;
+  // = TH, TW for P >= 0): overlapping pools recompute the shared conv rows
+  // instead of sending the pre-pool map through HBM.
+  int pw = 0, ph = 0, ps = 1, PHo = 0, PWo = 0, tsy = 0, tsx = 0;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -191,7 +205,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
 
   extern __shared__ float4 smem_raw[];
   float* smem = reinterpret_cast<float*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * Cfg::STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::RING);
   uint64_t* empty = full + NS;
 
   const int tid = threadIdx.x;
@@ -212,7 +226,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 33);  // 32 cp.async lane arrivals + the TMA expect_tx arrival
-      mbar_init(&empty[s], WPC);
+      mbar_init(&empty[s], SCONV_EMPTY_ALL_LANES ? WPC * 32 : WPC);
     }
   }
   __syncthreads();
@@ -221,7 +235,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
     // ------------------------------ producer ------------------------------
     const size_t plane = static_cast<size_t>(H) * W;
     if constexpr (Cfg::PAIR) {
-      if ((W & 1) == 0) {  // warp-uniform: 8-byte aligned cell pairs
+      // warp-uniform: 8-byte aligned cell pairs (every window row starts on
+      // an even column; general-pool tiles may step by an odd stride)
+      if ((W & 1) == 0 && ((a.tsx * S) & 1) == 0) {
         int src_off[Cfg::PAIRS_PER_LANE];
         int dst_off[Cfg::PAIRS_PER_LANE];
         int bytes[Cfg::PAIRS_PER_LANE];
@@ -233,7 +249,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
           const int t = cta * WPC + wi;
           const int n = t / a.tiles_per_img, tt = t - n * a.tiles_per_img;
           const int ty = tt / a.tiles_x, tx = tt - ty * a.tiles_x;
-          const int iy = ty * TH * S + Y, ix = tx * TW * S + X;
+          const int iy = ty * a.tsy * S + Y, ix = tx * a.tsx * S + X;
           const bool ok = q < Cfg::PAIRS && t < a.total_tiles && iy < H && ix < W;
           bytes[e] = ok ? (ix + 1 < W ? 8 : 4) : 0;
           src_off[e] = ok ? static_cast<int>((static_cast<size_t>(n) * C * H + iy) * W + ix) : 0;
@@ -279,7 +295,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
       const int t = cta * WPC + wi;
       const int n = t / a.tiles_per_img, tt = t - n * a.tiles_per_img;
       const int ty = tt / a.tiles_x, tx = tt - ty * a.tiles_x;
-      const int iy = ty * TH * S + Y, ix = tx * TW * S + X;
+      const int iy = ty * a.tsy * S + Y, ix = tx * a.tsx * S + X;
       ok[e] = q < Cfg::CELLS && t < a.total_tiles && iy < H && ix < W;
       src_off[e] = ok[e] ? static_cast<int>((static_cast<size_t>(n) * C * H + iy) * W + ix) : 0;
       dst_off[e] = (wi * CC) * PATCH + Y * PITCH + X;
@@ -356,14 +372,60 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
                                                                                 m1);
       }
     }
+#if SCONV_EMPTY_ALL_LANES
+    mbar_arrive(&empty[s]);  // every lane releases its own reads (count WPC * 32)
+#else
+    // lane 0 releases the stage for the warp: __syncwarp orders the other
+    // lanes' shared-memory reads before its mbarrier.arrive (release), and
+    // the producer's try_wait (acquire) orders them before its next copies.
+    // (compute-sanitizer racecheck does not follow this chain and reports the
+    // copies as WAR hazards; built with SCONV_EMPTY_ALL_LANES=1 every lane
+    // arrives and racecheck is clean: profiles/r02/sanitizer.md.)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+#endif
+  }
+  if constexpr (P < 0) {
+    // every consumer (active or not) has released its last stage: the ring
+    // is free once the producer's copies have all landed, which the last
+    // `full` wait of each consumer already observed
+    asm volatile("bar.sync 1, %0;" ::"r"(WPC * 32) : "memory");
   }
   if (!active) return;
 
   // ---- epilogue ------------------------------------------------------------
-  const int oy0 = ty * TH, ox0 = tx * TW;
-  if constexpr (P == 0) {
+  const int oy0 = ty * a.tsy, ox0 = tx * a.tsx;
+  if constexpr (P < 0) {
+    // Any pool (pecr_conv_pool, src/pecr.cpp:147-167): the warp's conv tile
+    // goes to its slice of the (now idle) ring, then each lane folds the
+    // pool windows of its own channels in window raster order -- max from
+    // +0 (ReLU folded), or the mean of max(v, 0) -- with no pre-pool value
+    // leaving the SM.
+    float* eb = smem + warp * (TH * TW * KT);
+#pragma unroll
+    for (int u = 0; u < TH; ++u)
+#pragma unroll
+      for (int v = 0; v < TW; ++v)
+#pragma unroll
+        for (int r = 0; r < R; ++r) eb[(u * TW + v) * KT + ws_lane_chan<R>(lane, r)] = acc[u][v][r];
+    __syncwarp();
+    const int pm = a.mode;
+    const int PTH = (TH - a.ph) / a.ps + 1, PTW = (TW - a.pw) / a.ps + 1;
+    const int py0 = ty * PTH, px0 = tx * PTW;
+    for (int r = 0; r < R; ++r) {
+      const int ch = ws_lane_chan<R>(lane, r), kk = k0 + ch;
+      if (kk >= K) continue;
+      float* dst = a.y + (static_cast<size_t>(n) * K + kk) * a.PHo * a.PWo;
+      for (int py = 0; py < PTH && py0 + py < a.PHo; ++py)
+        for (int px = 0; px < PTW && px0 + px < a.PWo; ++px) {
+          PoolFold f;
+          const float* wb = eb + (py * a.ps * TW + px * a.ps) * KT + ch;
+          for (int du = 0; du < a.ph; ++du)
+            for (int dv = 0; dv < a.pw; ++dv) f.add(wb[(du * TW + dv) * KT], pm);
+          dst[(py0 + py) * a.PWo + px0 + px] = f.result(pm, a.ph * a.pw);
+        }
+    }
+  } else if constexpr (P == 0) {
     if (a.mode) relu_tile(acc);  // fused Activation::kRelu (forward)
     const bool vec = (TW % 4 == 0) && (a.OW % 4 == 0);
 #pragma unroll

@@ -27,7 +27,10 @@ struct SmallCArgs {
   float* y;         // [N][K][OH][OW] or pooled [N][K][OH/2][OW/2]
   int N, C, H, W, K, Kp, OH, OW;
   int tiles_x, tiles_per_img, total_tiles;
-  int mode;         // P == 2: pool mode; P == 0: fused ReLU flag
+  int mode;         // P != 0: pool mode; P == 0: fused ReLU flag
+  // P == -1 (any pool): pool geometry, pooled map, conv-output tile strides
+  // (see WsArgs in ecr_ws.cuh); P >= 0: tsy = tsx = 4
+  int pw = 0, ph = 0, ps = 1, PHo = 0, PWo = 0, tsy = 4, tsx = 4;
 };
 
 template <int P, bool FAST>
@@ -40,7 +43,7 @@ __global__ void __launch_bounds__(256, P == 0 ? 4 : 3) ecr_smallc_kernel(const S
   const int k0 = blockIdx.y * KT;
   const int n = t / a.tiles_per_img, tt = t - n * a.tiles_per_img;
   const int ty = tt / a.tiles_x, tx = tt - ty * a.tiles_x;
-  const int oy0 = ty * TH, ox0 = tx * TW;
+  const int oy0 = ty * a.tsy, ox0 = tx * a.tsx;
 
   // lane l stages window cells l and l + 32 (cell q -> (q / 6, q % 6))
   const int q1 = lane + 32;
@@ -86,7 +89,35 @@ __global__ void __launch_bounds__(256, P == 0 ? 4 : 3) ecr_smallc_kernel(const S
     __syncwarp();  // the slot is rewritten by the next channel
   }
 
-  if constexpr (P == 0) {
+  if constexpr (P < 0) {
+    // any pool geometry: the conv tile goes through the warp's slice of shared
+    // memory and each lane folds the pool windows of its channels in window
+    // raster order (pecr_conv_pool, src/pecr.cpp:147-167)
+    __shared__ float ptile[8][TH * TW * KT];
+    float* eb = ptile[warp];
+#pragma unroll
+    for (int u = 0; u < TH; ++u)
+#pragma unroll
+      for (int v = 0; v < TW; ++v)
+#pragma unroll
+        for (int r = 0; r < R; ++r) eb[(u * TW + v) * KT + lane * R + r] = acc[u][v][r];
+    __syncwarp();
+    const int PTH = (TH - a.ph) / a.ps + 1, PTW = (TW - a.pw) / a.ps + 1;
+    const int py0 = ty * PTH, px0 = tx * PTW;
+    for (int r = 0; r < R; ++r) {
+      const int ch = lane * R + r, kk = k0 + ch;
+      if (kk >= a.K) continue;
+      float* dst = a.y + (static_cast<size_t>(n) * a.K + kk) * a.PHo * a.PWo;
+      for (int py = 0; py < PTH && py0 + py < a.PHo; ++py)
+        for (int px = 0; px < PTW && px0 + px < a.PWo; ++px) {
+          PoolFold f;
+          const float* wb = eb + (py * a.ps * TW + px * a.ps) * KT + ch;
+          for (int du = 0; du < a.ph; ++du)
+            for (int dv = 0; dv < a.pw; ++dv) f.add(wb[(du * TW + dv) * KT], a.mode);
+          dst[(py0 + py) * a.PWo + px0 + px] = f.result(a.mode, a.ph * a.pw);
+        }
+    }
+  } else if constexpr (P == 0) {
     if (a.mode) relu_tile(acc);  // fused Activation::kRelu (forward)
     // When the CTA's 8 tiles are one 32-wide strip of a row band, the tile is
     // transposed through shared memory so every warp store writes whole

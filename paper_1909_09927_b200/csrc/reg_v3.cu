@@ -6,7 +6,12 @@ namespace host {
 
 // which ws config (0 = none); P is 0 (ECR) or 2 (PECR 2x2/2)
 bool ws_applies(int id, int K, int kh, int kw, int S, int P) {
-  if (!(P == 0 || P == 2) || K < 32) return false;
+  if (K < 32) return false;
+  if (id >= 18 && id <= 20) {  // general-pool configs (P == -1 only)
+    if (P != -1 || S != 1) return false;
+    return id == 18 ? (kh == 3 && kw == 3) : id == 19 ? (kh == 5 && kw == 5) : (kh == 1 && kw == 1);
+  }
+  if (!(P == 0 || P == 2)) return false;
   if (id == 11) return kh == 3 && kw == 3 && S == 2;
   if (id == 12) return kh == 3 && kw == 3 && S == 3;
   if (S != 1) return false;
@@ -70,12 +75,29 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4, lon
   return (C >= 128 && tiles4 >= 148L * 10) ? 1 : 5;
 }
 
+// The general-pool config for a window / pool geometry (0 = none: the pool
+// then runs as conv + pecr_pool_fold_kernel): the conv tile must hold at
+// least one whole pool window.
+int pick_ws_pool(int K, int kh, int kw, int S, int pw, int ph) {
+  if (K < 32 || S != 1) return 0;
+  if (kh == 3 && kw == 3) return (pw <= WsR::TW && ph <= WsR::TH) ? 18 : 0;
+  if (kh == 5 && kw == 5) return (pw <= WsS::TW && ph <= WsS::TH) ? 19 : 0;
+  if (kh == 1 && kw == 1) return (pw <= WsT::TW && ph <= WsT::TH) ? 20 : 0;
+  return 0;
+}
+
 // Plan of a v3 launch: kernel id 100 + registry index; grid_x counts CTAs of
 // WPC warp tiles over the flat (image, tile) list, grid_z is 1.
 namespace {
 template <class Cfg>
-void plan_ws_t(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
-  const long tiles = long((OH + Cfg::TH - 1) / Cfg::TH) * ((OW + Cfg::TW - 1) / Cfg::TW) * N;
+void plan_ws_t(sconv_launch_plan* p, int which, int N, int K, int OH, int OW, int pw, int ph,
+               int ps) {
+  long tiles = long((OH + Cfg::TH - 1) / Cfg::TH) * ((OW + Cfg::TW - 1) / Cfg::TW) * N;
+  if (Cfg::P < 0 && pw > 0) {  // tiles of whole pool windows over the pooled map
+    const int pth = (Cfg::TH - ph) / ps + 1, ptw = (Cfg::TW - pw) / ps + 1;
+    const int PHo = (OH - ph) / ps + 1, PWo = (OW - pw) / ps + 1;
+    tiles = long((PHo + pth - 1) / pth) * ((PWo + ptw - 1) / ptw) * N;
+  }
   p->kernel = 100 + which;
   p->grid_x = static_cast<int>((tiles + Cfg::WPC - 1) / Cfg::WPC) * ((K + Cfg::KT - 1) / Cfg::KT);
   p->grid_y = 1;
@@ -89,24 +111,27 @@ void plan_ws_t(sconv_launch_plan* p, int which, int N, int K, int OH, int OW) {
 
 }  // namespace
 
-void plan_ws(sconv_launch_plan* out, int ws, int n, int k, int OH, int OW) {
+void plan_ws(sconv_launch_plan* out, int ws, int n, int k, int OH, int OW, int pw, int ph, int ps) {
   switch (ws) {
-    case 1: plan_ws_t<WsA<0>>(out, ws, n, k, OH, OW); break;
-    case 2: plan_ws_t<WsB<0>>(out, ws, n, k, OH, OW); break;
-    case 4: plan_ws_t<WsD<0>>(out, ws, n, k, OH, OW); break;
-    case 5: plan_ws_t<WsE<0>>(out, ws, n, k, OH, OW); break;
-    case 6: plan_ws_t<WsF<0>>(out, ws, n, k, OH, OW); break;
-    case 7: plan_ws_t<WsG<0>>(out, ws, n, k, OH, OW); break;
-    case 8: plan_ws_t<WsH<0>>(out, ws, n, k, OH, OW); break;
-    case 9: plan_ws_t<WsI<0>>(out, ws, n, k, OH, OW); break;
-    case 10: plan_ws_t<WsJ<0>>(out, ws, n, k, OH, OW); break;
-    case 11: plan_ws_t<WsK<0>>(out, ws, n, k, OH, OW); break;
-    case 12: plan_ws_t<WsL<0>>(out, ws, n, k, OH, OW); break;
-    case 14: plan_ws_t<WsN<0>>(out, ws, n, k, OH, OW); break;
-    case 15: plan_ws_t<WsO<0>>(out, ws, n, k, OH, OW); break;
-    case 16: plan_ws_t<WsP<0>>(out, ws, n, k, OH, OW); break;
-    case 17: plan_ws_t<WsQ<0>>(out, ws, n, k, OH, OW); break;
-    default: plan_ws_t<WsC<0>>(out, ws, n, k, OH, OW); break;
+    case 18: plan_ws_t<WsR>(out, ws, n, k, OH, OW, pw, ph, ps); return;
+    case 19: plan_ws_t<WsS>(out, ws, n, k, OH, OW, pw, ph, ps); return;
+    case 20: plan_ws_t<WsT>(out, ws, n, k, OH, OW, pw, ph, ps); return;
+    case 1: plan_ws_t<WsA<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 2: plan_ws_t<WsB<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 4: plan_ws_t<WsD<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 5: plan_ws_t<WsE<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 6: plan_ws_t<WsF<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 7: plan_ws_t<WsG<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 8: plan_ws_t<WsH<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 9: plan_ws_t<WsI<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 10: plan_ws_t<WsJ<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 11: plan_ws_t<WsK<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 12: plan_ws_t<WsL<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 14: plan_ws_t<WsN<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 15: plan_ws_t<WsO<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 16: plan_ws_t<WsP<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    case 17: plan_ws_t<WsQ<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
+    default: plan_ws_t<WsC<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
   }
 }
 

@@ -20,6 +20,7 @@
 #include "host/internal.h"
 #include "kernels/format.cuh"
 #include "kernels/generic.cuh"
+#include "kernels/ingest.cuh"
 #include "kernels/smallc.cuh"
 
 using namespace sconv_cu;
@@ -152,8 +153,8 @@ struct KernelChoice {
   bool smallc = false;      // ecr_smallc_kernel (C <= 4)
   int ws = 0;               // v3 warp-specialised config id (reg_v3.inc)
   int which = 0;            // v2 tiled config id (reg_v2.cu)
-  bool pool_after = false;  // PECR pool the epilogue does not fuse: conv, then pecr_pool_fold_kernel
-  int P = 0;                // pool extent fused into the conv epilogue (2) or 0
+  bool pool_after = false;  // PECR pool no epilogue fuses: conv, then pecr_pool_fold_kernel
+  int P = 0;                // epilogue: 2 = fused 2x2/2 pool, -1 = fused general pool, 0 = none
   bool tiled() const { return smallc || ws || which; }
 };
 
@@ -174,14 +175,23 @@ int choose_kernel(sconv_cu_ctx* ctx, int n, int c, int k, int kh, int kw, int st
     ch.smallc = tileable && (forced == 'M' || (!forced && c <= 4));
     ch.ws = ch.smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, Pk, tiles4, tiles2);
     ch.which = ch.ws || ch.smallc ? 0 : pick_tiled(k, kh, kw, stride, Pk);
-    // PECR with a pool the fused epilogue does not cover (anything but
-    // 2x2/2): a tiled kernel computes the conv into a workspace, then
-    // pecr_pool_fold_kernel folds the pools (the pre-pool map does reach HBM).
+    // PECR with a pool other than 2x2/2: the kernels whose tiles hold whole
+    // pool windows fold it in the epilogue (P = -1); a geometry none of them
+    // fits (pool larger than the conv tile, strided conv) falls back to a
+    // tiled conv into a workspace + pecr_pool_fold_kernel (the pre-pool map
+    // then does reach HBM).
     if (pecr && Pk != 2 && !ch.tiled() && !forced) {
-      ch.smallc = kh == 3 && kw == 3 && stride == 1 && k >= 32 && c <= 4;
-      ch.ws = ch.smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0, tiles4, tiles2);
-      ch.which = ch.smallc || ch.ws ? 0 : pick_tiled(k, kh, kw, stride, 0);
-      ch.pool_after = ch.tiled();
+      if (kh == 3 && kw == 3 && stride == 1 && k >= 32 && c <= 4 && pw <= 4 && ph <= 4) {
+        ch.smallc = true;
+        ch.P = -1;
+      } else if ((ch.ws = pick_ws_pool(k, kh, kw, stride, pw, ph)) != 0) {
+        ch.P = -1;
+      } else {
+        ch.smallc = kh == 3 && kw == 3 && stride == 1 && k >= 32 && c <= 4;
+        ch.ws = ch.smallc ? 0 : pick_ws(k, c, OW, kh, kw, stride, 0, tiles4, tiles2);
+        ch.which = ch.smallc || ch.ws ? 0 : pick_tiled(k, kh, kw, stride, 0);
+        ch.pool_after = ch.tiled();
+      }
     }
     if (forced && forced != 'M') {
       if (forced >= 1 && forced <= kNumCfgs) {
@@ -189,27 +199,44 @@ int choose_kernel(sconv_cu_ctx* ctx, int n, int c, int k, int kh, int kw, int st
           ch.which = forced;
           ch.ws = 0;
         }
-      } else if (forced >= 'A' && forced <= 'Q') {
-        if (!ws_applies(forced - 'A' + 1, k, kh, kw, stride, Pk))
+      } else if (forced >= 'A' && forced <= 'T') {
+        const int id = forced - 'A' + 1;
+        const bool general = id >= 18;
+        if (general ? !(pecr && Pk != 2 && pick_ws_pool(k, kh, kw, stride, pw, ph) == id)
+                    : !ws_applies(id, k, kh, kw, stride, Pk))
           return fail(ctx, SCONV_ERR_ARG, "forced kernel %c does not apply to this shape", forced);
-        ch.ws = forced - 'A' + 1;
+        ch.ws = id;
         ch.which = 0;
+        ch.smallc = false;
+        ch.P = general ? -1 : 0;
       } else {
         return fail(ctx, SCONV_ERR_ARG, "unknown forced kernel id %d", forced);
       }
     }
   }
-  ch.P = ch.tiled() && !ch.pool_after ? (Pk == 2 ? 2 : 0) : 0;
+  if (ch.P != -1) ch.P = ch.tiled() && !ch.pool_after && Pk == 2 ? 2 : 0;
   *out = ch;
   return SCONV_OK;
 }
 
+// Warp tiles of the small-C kernel per image: 4x4 conv outputs, or (P = -1)
+// the tiles of whole pool windows.
+long smallc_tiles(const KernelChoice& ch, int OH, int OW, int pw, int ph, int ps) {
+  if (ch.P < 0) {
+    const int pth = (4 - ph) / ps + 1, ptw = (4 - pw) / ps + 1;
+    const int PHo = (OH - ph) / ps + 1, PWo = (OW - pw) / ps + 1;
+    return long((PHo + pth - 1) / pth) * ((PWo + ptw - 1) / ptw);
+  }
+  return long((OH + 3) / 4) * ((OW + 3) / 4);
+}
+
 // CTAs one launch of `nb` images takes (chunk sizing below).
-long ctas_for(const KernelChoice& ch, int nb, int k, int OH, int OW, size_t y_img) {
+long ctas_for(const KernelChoice& ch, int nb, int k, int OH, int OW, size_t y_img, int pw, int ph,
+              int ps) {
   sconv_launch_plan pl{};
-  if (ch.smallc) return long((size_t(nb) * ((OH + 3) / 4) * ((OW + 3) / 4) + 7) / 8) * ((k + 63) / 64);
+  if (ch.smallc) return (nb * smallc_tiles(ch, OH, OW, pw, ph, ps) + 7) / 8 * ((k + 63) / 64);
   if (ch.ws) {
-    plan_ws(&pl, ch.ws, nb, k, OH, OW);
+    plan_ws(&pl, ch.ws, nb, k, OH, OW, pw, ph, ps);
     return long(pl.grid_x) * pl.grid_y * pl.grid_z;
   }
   if (ch.which) {
@@ -225,7 +252,7 @@ long ctas_for(const KernelChoice& ch, int nb, int k, int OH, int OW, size_t y_im
 // pointers: one chunk, unless a launch limit cuts it.
 std::vector<std::pair<int, int>> plan_chunks(const sconv_cu_ctx* ctx, const KernelChoice& ch, int n,
                                              int k, int OH, int OW, size_t x_elems, size_t y_elems,
-                                             bool dev, bool async) {
+                                             bool dev, bool async, int pw, int ph, int ps) {
   static const int chunk_env = [] {  // dev override (tools/e2e_probe.py)
     const char* e = std::getenv("SCONV_CHUNKS");
     return e ? std::atoi(e) : 0;
@@ -247,7 +274,7 @@ std::vector<std::pair<int, int>> plan_chunks(const sconv_cu_ctx* ctx, const Kern
       // otherwise be more than 16 chunks (e.g. conv4_2: 28 CTAs per image ->
       // 10-image chunks = 0.95 wave; 11 would spill 12 CTAs into a 2nd wave;
       // tools/e2e_probe.py: conv4_2 loses 20% at 4-image chunks)
-      const double per_img = std::max(1.0, double(ctas_for(ch, n, k, OH, OW, y_img)) / n);
+      const double per_img = std::max(1.0, double(ctas_for(ch, n, k, OH, OW, y_img, pw, ph, ps)) / n);
       const int wave = std::max(1, static_cast<int>(2.0 * ctx->num_sms / per_img));
       const int chunk = wave * std::max(1, (n + 16 * wave - 1) / (16 * wave));
       nchunk = std::max(1, (n + chunk - 1) / chunk);
@@ -304,11 +331,22 @@ int launch_chunk(sconv_cu_ctx* ctx, const KernelChoice& ch, cudaStream_t cs, con
   const int model = ch.pool_after ? 0 : mode;
   if (ch.smallc) {
     SmallCArgs a{dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, model};
-    a.tiles_x = (OW + 3) / 4;
-    a.tiles_per_img = a.tiles_x * ((OH + 3) / 4);
+    if (ch.P < 0) {  // tiles of whole pool windows
+      const int pth = (4 - ph) / ps + 1, ptw = (4 - pw) / ps + 1;
+      a.pw = pw, a.ph = ph, a.ps = ps, a.PHo = PHo, a.PWo = PWo;
+      a.tsy = pth * ps, a.tsx = ptw * ps;
+      a.tiles_x = (PWo + ptw - 1) / ptw;
+      a.tiles_per_img = a.tiles_x * ((PHo + pth - 1) / pth);
+    } else {
+      a.tiles_x = (OW + 3) / 4;
+      a.tiles_per_img = a.tiles_x * ((OH + 3) / 4);
+    }
     a.total_tiles = a.tiles_per_img * nb;
     const dim3 grid((a.total_tiles + 7) / 8, (k + 63) / 64);
-    if (ch.P == 2)
+    if (ch.P < 0)
+      fast ? ecr_smallc_kernel<-1, true><<<grid, 256, 0, cs>>>(a)
+           : ecr_smallc_kernel<-1, false><<<grid, 256, 0, cs>>>(a);
+    else if (ch.P == 2)
       fast ? ecr_smallc_kernel<2, true><<<grid, 256, 0, cs>>>(a)
            : ecr_smallc_kernel<2, false><<<grid, 256, 0, cs>>>(a);
     else
@@ -317,6 +355,7 @@ int launch_chunk(sconv_cu_ctx* ctx, const KernelChoice& ch, cudaStream_t cs, con
     TRY(finish_launch(ctx, "ecr_smallc_kernel"));
   } else if (ch.ws) {
     WsArgs a{dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, model};
+    if (ch.P < 0) a.pw = pw, a.ph = ph, a.ps = ps, a.PHo = PHo, a.PWo = PWo;
     TRY(fast ? launch_ws_fast(ctx, ch.ws, ch.P, a) : launch_ws_exact(ctx, ch.ws, ch.P, a));
   } else if (ch.which) {
     TiledArgs a{dx, wt, dconv, c, h, w, k, OH, OW, 0, model};
@@ -342,10 +381,29 @@ int launch_chunk(sconv_cu_ctx* ctx, const KernelChoice& ch, cudaStream_t cs, con
   return SCONV_OK;
 }
 
-// Shared body of the fused ECR / PECR entries.
+// A batch in the compressed-ingest layout (include/sconv_cuda.h).
+struct PackedIn {
+  const uint32_t* bits;
+  const int64_t* base;
+  const float* values;
+};
+
+// Expands images [n0, n0 + nb) of a packed batch into dense x (device).
+// bits / base point at image n0's; values[0] is the absolute offset value0.
+int expand_chunk(sconv_cu_ctx* ctx, cudaStream_t cs, const uint32_t* bits, const int64_t* base,
+                 const float* values, int64_t value0, int nb, int64_t elems, float* x) {
+  int64_t words = (elems + 31) / 32, blocks = (words + 31) / 32;
+  ExpandArgs ea{bits, base, values, value0, nb, elems, words, blocks, x};
+  const size_t warps = size_t(nb) * blocks;
+  expand_packed_kernel<<<grid_for(warps * 32, 256, ctx->num_sms * 8), 256, 0, cs>>>(ea);
+  return finish_launch(ctx, "expand_packed_kernel");
+}
+
+// Shared body of the fused ECR / PECR entries.  `pk`: the input comes in the
+// compressed-ingest layout instead of dense x (x unused).
 int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, const float* filt,
                int k, int kh, int kw, int stride, int pw, int ph, int ps, int mode, float* y,
-               uint64_t* muls, uint64_t* adds, unsigned flags) {
+               uint64_t* muls, uint64_t* adds, unsigned flags, const PackedIn* pk = nullptr) {
   if (!ctx) return fail(nullptr, SCONV_ERR_ARG, "null context");
   const bool pecr = pw > 0;
   if (n < 0 || k < 0) return fail(ctx, SCONV_ERR_SHAPE, "negative batch or filter count");
@@ -366,7 +424,10 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
   // the copies to overlap).
   const bool host_async = async && !dev;
   if (n == 0 || k == 0) return SCONV_OK;
-  if (!x || !filt || !y) return fail(ctx, SCONV_ERR_ARG, "null tensor pointer");
+  const bool packed = pk != nullptr;
+  if (packed) x = nullptr;
+  if ((!packed && !x) || (packed && (!pk->bits || !pk->base)) || !filt || !y)
+    return fail(ctx, SCONV_ERR_ARG, "null tensor pointer");
   if (dev && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15))
     return fail(ctx, SCONV_ERR_ARG, "device x and y must be 16-byte aligned");
   KernelChoice ch;
@@ -381,13 +442,28 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
 
   DeviceGuard guard(ctx->device);
   const std::vector<std::pair<int, int>> chunks =
-      plan_chunks(ctx, ch, n, k, OH, OW, x_elems, y_elems, dev, async);
+      plan_chunks(ctx, ch, n, k, OH, OW, x_elems, y_elems, dev, async, pw, ph, ps);
   const int nchunk = static_cast<int>(chunks.size());
   int per = 0;
   for (const auto& cp : chunks) per = std::max(per, cp.second);
   const size_t x_img = size_t(c) * h * w, y_img = y_elems / size_t(n);
   const int nbuf = dev ? 0 : std::min(nchunk, 3);
   const bool piped = !dev && nchunk > 1;
+  // compressed ingest: per-image bitmap words / block offsets, and (host
+  // pointers) the value count of every chunk, read off the host offsets
+  const int64_t pk_words = (int64_t(x_img) + 31) / 32, pk_blocks = (pk_words + 31) / 32;
+  std::vector<int64_t> chunk_v0(nchunk, 0), chunk_nv(nchunk, 0);
+  int64_t pk_vmax = 0;
+  if (packed && !dev) {
+    for (int ci = 0; ci < nchunk; ++ci) {
+      const int n0 = chunks[ci].first, nb = chunks[ci].second;
+      chunk_v0[ci] = pk->base[int64_t(n0) * (pk_blocks + 1)];
+      chunk_nv[ci] = pk->base[int64_t(n0 + nb - 1) * (pk_blocks + 1) + pk_blocks] - chunk_v0[ci];
+      if (chunk_nv[ci] < 0) return fail(ctx, SCONV_ERR_FORMAT, "packed offsets decrease");
+      if (chunk_nv[ci] > 0 && !pk->values) return fail(ctx, SCONV_ERR_ARG, "null packed values");
+      pk_vmax = std::max(pk_vmax, chunk_nv[ci]);
+    }
+  }
 
   // Filters for SCONV_F_CACHE_FILTERS: the context's copy, made on first use.
   sconv_filter_entry* fe = cache ? find_filters(ctx, filt, !dev, k, c, kh * kw, need_wt ? Kp : 0) : nullptr;
@@ -413,10 +489,17 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     else CK(cudaEventSynchronize(ctx->ev_hws[ar.host]));
   }
   size_t i_x[3] = {0, 0, 0}, i_y[3] = {0, 0, 0}, i_pix[3] = {0, 0, 0};
+  size_t i_pb[3] = {0, 0, 0}, i_pbase[3] = {0, 0, 0}, i_pv[3] = {0, 0, 0};
   for (int b = 0; b < nbuf; ++b) {
     i_x[b] = ar.add(size_t(per) * x_img * 4);
     i_y[b] = ar.add(size_t(per) * y_img * 4);
+    if (packed) {  // the chunk as it crosses PCIe
+      i_pb[b] = ar.add(size_t(per) * pk_words * 4);
+      i_pbase[b] = ar.add(size_t(per) * (pk_blocks + 1) * 8);
+      i_pv[b] = ar.add(size_t(std::max<int64_t>(pk_vmax, 1)) * 4);
+    }
   }
+  if (dev && packed) i_x[0] = ar.add(size_t(per) * x_img * 4);  // expansion target
   const size_t i_w = dev || fe ? 0 : ar.add(w_elems * 4);
   const size_t i_wt = need_wt && !fe ? ar.add(size_t(Kp) * c * kh * kw * 4) : 0;
   for (int b = 0; b < (counters ? std::max(nbuf, 1) : 0); ++b) i_pix[b] = ar.add(size_t(per) * h * w * 4);
@@ -477,19 +560,39 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     if (nb <= 0) break;
     const int b = dev ? 0 : ci % nbuf;
     cudaStream_t cs = st;
-    const float* dx = dev ? x + size_t(n0) * x_img : reinterpret_cast<float*>(p[i_x[b]]);
+    float* xslot = (!dev || packed) ? reinterpret_cast<float*>(p[i_x[b]]) : nullptr;
+    const float* dx = (dev && !packed) ? x + size_t(n0) * x_img : xslot;
     float* dy = dev ? y + size_t(n0) * y_img : reinterpret_cast<float*>(p[i_y[b]]);
     float* dconv = ch.pool_after ? reinterpret_cast<float*>(p[i_conv]) : dy;  // conv kernels write here
     if (!dev) {
       cudaStream_t hs = piped ? ctx->h2d : st;
       if (piped && ci >= nbuf) CK(cudaStreamWaitEvent(hs, ctx->ev_comp[b], 0));  // x slot free
-      CK(cudaMemcpyAsync(const_cast<float*>(dx), x + size_t(n0) * x_img, size_t(nb) * x_img * 4,
-                         cudaMemcpyHostToDevice, hs));
+      if (packed) {  // bitmap, block offsets and nonzeros of the chunk's images
+        CK(cudaMemcpyAsync(p[i_pb[b]], pk->bits + int64_t(n0) * pk_words,
+                           size_t(nb) * pk_words * 4, cudaMemcpyHostToDevice, hs));
+        CK(cudaMemcpyAsync(p[i_pbase[b]], pk->base + int64_t(n0) * (pk_blocks + 1),
+                           size_t(nb) * (pk_blocks + 1) * 8, cudaMemcpyHostToDevice, hs));
+        if (chunk_nv[ci] > 0)
+          CK(cudaMemcpyAsync(p[i_pv[b]], pk->values + chunk_v0[ci], size_t(chunk_nv[ci]) * 4,
+                             cudaMemcpyHostToDevice, hs));
+      } else {
+        CK(cudaMemcpyAsync(const_cast<float*>(dx), x + size_t(n0) * x_img, size_t(nb) * x_img * 4,
+                           cudaMemcpyHostToDevice, hs));
+      }
       if (piped) {
         CK(cudaEventRecord(ctx->ev_in[b], hs));
         CK(cudaStreamWaitEvent(cs, ctx->ev_in[b], 0));
         if (ci >= nbuf) CK(cudaStreamWaitEvent(cs, ctx->ev_out[b], 0));  // y slot drained
       }
+    }
+    if (packed) {  // compressed ingest: dense chunk rebuilt in HBM, then the conv
+      if (dev)
+        TRY(expand_chunk(ctx, cs, pk->bits + int64_t(n0) * pk_words,
+                         pk->base + int64_t(n0) * (pk_blocks + 1), pk->values, 0, nb, x_img, xslot));
+      else
+        TRY(expand_chunk(ctx, cs, reinterpret_cast<uint32_t*>(p[i_pb[b]]),
+                         reinterpret_cast<int64_t*>(p[i_pbase[b]]), reinterpret_cast<float*>(p[i_pv[b]]),
+                         chunk_v0[ci], nb, x_img, xslot));
     }
     TRY(launch_chunk(ctx, ch, cs, dx, dw, wt, dconv, dy, nb, c, h, w, k, Kp, kh, kw, stride, OH, OW,
                      pw, ph, ps, mode, PHo, PWo, pecr, fast));
@@ -756,7 +859,7 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
   const bool smallc = ch.smallc;
   const int ws = ch.ws, which = ch.which;
   if (smallc) {
-    const long tiles = long(n) * ((OH + 3) / 4) * ((OW + 3) / 4);
+    const long tiles = long(n) * smallc_tiles(ch, OH, OW, pool_w, pool_h, pool_stride);
     out->kernel = 300;
     out->grid_x = static_cast<int>((tiles + 7) / 8);
     out->grid_y = (k + 63) / 64;
@@ -766,7 +869,7 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
     out->tile_h = out->tile_w = 4;
     out->tile_k = 64;
   } else if (ws) {
-    plan_ws(out, ws, n, k, OH, OW);
+    plan_ws(out, ws, n, k, OH, OW, ch.P < 0 ? pool_w : 0, pool_h, pool_stride);
   } else if (which) {
     plan_for(out, which, n, k, OH, OW);
   } else {
@@ -1101,6 +1204,41 @@ int sconv_cu_pecr_conv_pool(sconv_cu_ctx* ctx, const float* x, int n, int c, int
     return fail(ctx, SCONV_ERR_CONFIG, "pack count arguments must be positive");
   return fused_conv(ctx, x, n, c, h, w, filters, k, kh, kw, stride, pool_w, pool_h, pool_stride,
                     mode, y, muls, adds, flags);
+}
+
+int sconv_cu_ecr_conv_packed(sconv_cu_ctx* ctx, const uint32_t* bits, const int64_t* base,
+                             const float* values, int n, int c, int h, int w, const float* filters,
+                             int k, int kh, int kw, int stride, float* y, uint64_t* muls,
+                             uint64_t* adds, unsigned flags) {
+  const PackedIn pk{bits, base, values};
+  return fused_conv(ctx, nullptr, n, c, h, w, filters, k, kh, kw, stride, 0, 0, 1, 0, y, muls, adds,
+                    flags, &pk);
+}
+
+int sconv_cu_pecr_conv_pool_packed(sconv_cu_ctx* ctx, const uint32_t* bits, const int64_t* base,
+                                   const float* values, int n, int c, int h, int w,
+                                   const float* filters, int k, int kh, int kw, int stride,
+                                   int pool_w, int pool_h, int pool_stride, int mode, float* y,
+                                   uint64_t* muls, uint64_t* adds, unsigned flags) {
+  if (pool_w < 1 || pool_h < 1)
+    return fail(ctx, SCONV_ERR_CONFIG, "pack count arguments must be positive");
+  const PackedIn pk{bits, base, values};
+  return fused_conv(ctx, nullptr, n, c, h, w, filters, k, kh, kw, stride, pool_w, pool_h,
+                    pool_stride, mode, y, muls, adds, flags, &pk);
+}
+
+int sconv_cu_unpack_maps(sconv_cu_ctx* ctx, const uint32_t* bits, const int64_t* base,
+                         const float* values, int n, int c, int h, int w, float* x,
+                         unsigned flags) {
+  if (!ctx) return fail(nullptr, SCONV_ERR_ARG, "null context");
+  if (n < 0 || c < 1 || h < 1 || w < 1) return fail(ctx, SCONV_ERR_SHAPE, "bad map dims");
+  if (n == 0) return SCONV_OK;
+  if (!(flags & SCONV_F_DEVICE)) return fail(ctx, SCONV_ERR_ARG, "sconv_cu_unpack_maps takes device pointers");
+  if (!bits || !base || !x) return fail(ctx, SCONV_ERR_ARG, "null pointer");
+  DeviceGuard guard(ctx->device);
+  TRY(expand_chunk(ctx, ctx->stream, bits, base, values, 0, n, int64_t(c) * h * w, x));
+  if (!(flags & SCONV_F_ASYNC)) CK(cudaStreamSynchronize(ctx->stream));
+  return SCONV_OK;
 }
 
 int sconv_cu_ecr_convert(sconv_cu_ctx* ctx, const float* x, int c, int h, int w,

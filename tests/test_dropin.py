@@ -84,3 +84,14 @@ def test_reference_cli_suite_on_gpu():
     r = _run("cli_dropin", {"SCONV_CUDA_MODE": "exact"})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert re.search(r"\| 0 failed \|", r.stdout)
+
+
+@pytest.mark.gpu
+def test_cuda_hpp_batched_entries():
+    """include/sconv/cuda.hpp (multichannel_conv / conv_pool / forward, batched
+    over the C ABI) against the unmodified reference compiled into the same
+    binary: bit-identical outputs, equal OpCounts, ForwardResult fields and
+    the reference's exception types."""
+    r = _run("cuda_hpp_test")
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "cuda_hpp_test: ok" in r.stdout

@@ -241,3 +241,62 @@ def test_misaligned_device_views(sc, orc):
     st = L.sconv_cu_ecr_conv(ctx.handle, xv.data_ptr(), 2, 8, 18, 18, wd.data_ptr(), 64, 3, 3, 1,
                              ov.data_ptr(), None, None, sc._native.F_DEVICE)
     assert st == 7  # SCONV_ERR_ARG
+
+
+# ---------------------------------------------------------------------------
+# compressed ingest: bitmap + packed nonzeros across PCIe, expanded on device
+# ---------------------------------------------------------------------------
+PACK_SHAPES = [
+    # n, c, h, w, k, sparsity, pool
+    (3, 16, 22, 22, 128, 0.7, None),
+    (5, 64, 30, 30, 64, 0.5, (2, 2, 2)),
+    (2, 3, 34, 34, 64, 0.7, None),          # C*H*W not a multiple of 1024
+    (4, 32, 17, 17, 64, 0.95, (3, 3, 2)),   # general pool
+    (2, 8, 12, 12, 64, 1.0, None),          # all-zero maps
+    (21, 128, 16, 16, 256, 0.7, (2, 2, 2)), # several host chunks
+]
+
+
+@pytest.mark.parametrize("shape", PACK_SHAPES, ids=[str(s) for s in PACK_SHAPES])
+def test_packed_ingest(sc, orc, shape):
+    """The packed entries give the dense entries' bits (EXACT and FAST) and the
+    oracle's, with host pointers (the chunked H2D ring) and device pointers."""
+    torch = pytest.importorskip("torch")
+    n, c, h, w, k, s, pool = shape
+    x = np.stack([orc.generate(h, w, c, s, 900 + i) for i in range(n)])
+    f = np.stack([orc.generate(3, 3, c, 0.0, 950 + j) for j in range(k)]) - np.float32(0.5)
+    p = sc.pack_maps(x)
+    assert p.nbytes < x.nbytes or s < 0.05
+    pc = None if pool is None else sc.PoolConfig(*pool)
+    if pc is None:
+        ref, rops = orc.ecr_conv(x, f, 1)
+        run = lambda xx, **kw: sc.ecr_conv_batched(xx, f if not kw.pop("dev", False) else fd, 1, **kw)
+    else:
+        ref, rops = orc.pecr_conv(x, f, 1, *pool, 0)
+        run = lambda xx, **kw: sc.pecr_conv_pool_batched(xx, f if not kw.pop("dev", False) else fd,
+                                                         1, pc, **kw)
+    fd = torch.from_numpy(f).cuda()
+    ops = sc.OpCount()
+    assert bits_equal(run(p, counters=ops), ref)
+    assert (ops.multiplications, ops.additions) == rops
+    assert bits_equal(run(p, fast=True), run(x, fast=True))
+    pd = p.to("cuda")
+    assert bits_equal(run(pd, dev=True).cpu().numpy(), ref)
+    xd = sc.unpack_maps(pd)
+    expect = np.where(x == 0, np.float32(0), x)   # -0 travels as +0
+    assert bits_equal(xd.cpu().numpy(), expect)
+
+
+def test_packed_async_host_calls(sc, orc):
+    """Asynchronous packed host calls back to back (the bench's e2e leg)."""
+    xs = [np.stack([orc.generate(18, 18, 32, 0.7, 10 * l + i) for i in range(6)]) for l in range(3)]
+    fs = [np.stack([orc.generate(3, 3, 32, 0.0, 500 + 10 * l + j) for j in range(64)]) - np.float32(0.5)
+          for l in range(3)]
+    ps = [sc.pack_maps(x) for x in xs]
+    outs = [np.empty((6, 64, 16, 16), np.float32) for _ in range(3)]
+    for _ in range(2):
+        for l in range(3):
+            sc.ecr_conv_batched(ps[l], fs[l], 1, out=outs[l], sync=False)
+        sc.synchronize(0)
+        for l in range(3):
+            assert bits_equal(outs[l], orc.ecr_conv(xs[l], fs[l], 1)[0])

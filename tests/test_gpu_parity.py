@@ -547,16 +547,31 @@ PSHAPES = [
     (1, 24, 14, 20, 128, 3, 1, (2, 3, 1), 0.5),   # non-square, stride 1
     (2, 3, 20, 20, 64, 3, 1, (3, 3, 3), 0.7),     # small C (smallc conv), 3x3/3
     (1, 20, 15, 15, 48, 5, 1, (3, 3, 2), 0.8),    # 5x5 conv, overlapping pool
+    (3, 128, 29, 29, 256, 3, 1, (3, 3, 2), 0.7),  # VGG-sized C/K, overlapping pool
+    (2, 3, 23, 23, 64, 3, 1, (3, 3, 2), 0.6),     # small C, overlapping pool
+    (2, 64, 13, 13, 96, 1, 1, (3, 3, 2), 0.7),    # 1x1 conv (inception), overlapping pool
+    (1, 32, 16, 12, 64, 3, 1, (6, 6, 2), 0.7),    # pool as large as the 6x6 conv tile
+    (1, 32, 19, 19, 64, 3, 1, (7, 7, 2), 0.7),    # pool larger than any tile: conv + fold
+    (2, 16, 23, 23, 64, 3, 2, (3, 3, 2), 0.7),    # strided conv: conv + fold
 ]
 
 
 @pytest.mark.parametrize("shape", PSHAPES, ids=[str(s) for s in PSHAPES])
 def test_pecr_other_pools(sc, orc, shape):
-    """Pools other than 2x2/2: conv by a tiled kernel, then the PECR fold --
-    bit-identical to the reference's pecr_conv_pool in EXACT mode."""
+    """Pools other than 2x2/2, fused: the tile covers whole pool windows and
+    the epilogue folds them (one kernel, no pre-pool map in HBM) -- except
+    geometries no tile fits, which run conv + pecr_pool_fold_kernel.  Bit-
+    identical to the reference's pecr_conv_pool in EXACT mode."""
     n, c, h, w, k, kk, s, (pw, ph, ps), sp = shape
     x, f = inputs(orc, n, c, h, w, k, kk, kk, sp, seed=(hash(shape) ^ 21) & 0xFFFF)
-    assert sc.launch_plan(n, c, h, w, k, kk, kk, s, sc.PoolConfig(pw, ph, ps))["kernel"] != 0
+    plan = sc.launch_plan(n, c, h, w, k, kk, kk, s, sc.PoolConfig(pw, ph, ps))
+    assert plan["kernel"] != 0
+    fused = s == 1 and (pw <= 4 if c <= 4 and kk == 3 else pw <= (6 if kk == 3 else 4))
+    ctx = sc.context(0)
+    l0 = ctx.launches
+    sc.pecr_conv_pool_batched(x, f, s, sc.PoolConfig(pw, ph, ps))
+    # filter re-layout + the conv kernel; + pecr_pool_fold_kernel when not fused
+    assert ctx.launches - l0 == (2 if fused else 3), plan
     for mode in (0, 1):
         pref, rops = orc.pecr_conv(x, f, s, pw, ph, ps, mode)
         pool = sc.PoolConfig(pw, ph, ps, sc.PoolMode(mode))

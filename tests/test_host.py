@@ -174,3 +174,45 @@ def test_product_does_not_touch_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h", ".hpp")) and "dropin" not in dirpath:
                 text = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", text).replace("oracle/_ref", ""), f
+
+
+def _pack_restated(x):
+    """numpy restatement of the compressed-ingest layout (include/sconv_cuda.h)."""
+    n = x.shape[0]
+    f = x.reshape(n, -1)
+    e = f.shape[1]
+    words = (e + 31) // 32
+    blocks = (words + 31) // 32
+    bits = np.zeros((n, words), np.uint32)
+    base = np.zeros((n, blocks + 1), np.int64)
+    vals, pos = [], 0
+    for i in range(n):
+        nz = f[i] != 0
+        for b in range(blocks):
+            base[i, b] = pos
+            pos += int(nz[b * 1024:(b + 1) * 1024].sum())
+        base[i, blocks] = pos
+        idx = np.nonzero(nz)[0]
+        np.bitwise_or.at(bits[i], idx // 32, (np.uint32(1) << (idx % 32).astype(np.uint32)))
+        vals.append(f[i][nz])
+    return bits, base, np.concatenate(vals) if vals else np.zeros(0, np.float32)
+
+
+@pytest.mark.parametrize("shape,s", [((3, 5, 7, 9), 0.6), ((2, 64, 34, 34), 0.7), ((1, 1, 1, 1), 0.0),
+                                     ((2, 3, 33, 31), 1.0), ((4, 2, 40, 40), 0.95)])
+def test_pack_maps_layout(sc, shape, s):
+    """sconv_pack_maps (host) against a numpy restatement of the layout:
+    bitmap, absolute 1024-element block offsets, values in element order;
+    -0.0 is a zero (ecr_convert's v != 0.0f, src/ecr.cpp:84)."""
+    rng = np.random.default_rng(sum(shape))
+    x = rng.random(shape, np.float32) + np.float32(0.01)
+    x[rng.random(shape) < s] = 0.0
+    x.reshape(-1)[:: 7] *= -1.0
+    if x.size > 3:
+        x.reshape(-1)[3] = -0.0
+    p = sc.pack_maps(x)
+    bits, base, vals = _pack_restated(x)
+    assert np.array_equal(p.bits, bits)
+    assert np.array_equal(p.base, base)
+    assert np.array_equal(p.values.view(np.uint32), vals.view(np.uint32))
+    assert p.nbytes == bits.nbytes + base.nbytes + vals.nbytes
