@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -22,6 +23,8 @@
 #include "kernels/generic.cuh"
 #include "kernels/ingest.cuh"
 #include "kernels/smallc.cuh"
+#include "kernels/smallc2.cuh"
+#include "host/tma.h"
 
 using namespace sconv_cu;
 using namespace sconv_cu::host;
@@ -151,6 +154,7 @@ int pack_count(sconv_cu_ctx* ctx, int in, int k, int cs, int p, int ps, int* out
 // for the launch (fused_conv) and the launch-plan query (sconv_cu_plan).
 struct KernelChoice {
   bool smallc = false;      // ecr_smallc_kernel (C <= 4)
+  bool sc2 = false;         // ... as the persistent ecr_smallc2_kernel (ECR, OW % 4 == 0)
   int ws = 0;               // v3 warp-specialised config id (reg_v3.inc)
   int which = 0;            // v2 tiled config id (reg_v2.cu)
   bool pool_after = false;  // PECR pool no epilogue fuses: conv, then pecr_pool_fold_kernel
@@ -215,6 +219,11 @@ int choose_kernel(sconv_cu_ctx* ctx, int n, int c, int k, int kh, int kw, int st
     }
   }
   if (ch.P != -1) ch.P = ch.tiled() && !ch.pool_after && Pk == 2 ? 2 : 0;
+  // plain ECR on a few channels: the persistent small-C kernel (smallc2.cuh)
+  // when its strips tile the map with whole float4 rows and the filters fit
+  // its shared-memory budget; forced 'M' keeps the per-tile kernel
+  static const bool sc2_off = std::getenv("SCONV_NO_SC2") != nullptr;  // dev A/B
+  ch.sc2 = ch.smallc && ch.P == 0 && !ch.pool_after && forced != 'M' && !sc2_off;
   *out = ch;
   return SCONV_OK;
 }
@@ -323,13 +332,112 @@ void free_filter_entry(sconv_filter_entry& e) {
   e.dev = e.wt = nullptr;
 }
 
+// The lanes-over-pixels small-C kernel reads its filters from the constant
+// bank (c_sc2_w).  A launch takes one of kSc2Slots slots per device, copies its
+// [C][9][64] K-block there on its stream (D2D), and records an event the next
+// user of the slot waits on, so launches on any streams / contexts never see
+// each other's filters.  A stream that is capturing a graph uses the
+// per-tile kernel instead (the slot's event would cross the capture).
+struct Sc2SlotTable {
+  std::mutex mu;
+  int next = 0;
+  cudaEvent_t ev[kSc2Slots] = {};
+  float* base = nullptr;  // device address of c_sc2_w (floats)
+};
+Sc2SlotTable& sc2_slots(int device) {
+  static Sc2SlotTable tables[64];
+  return tables[device & 63];
+}
+
+template <int C, bool FAST, bool RELU, bool TMA>
+int launch_smallc2_c(sconv_cu_ctx* ctx, cudaStream_t cs, SmallC2Args a, const float* wt,
+                     const CUtensorMap& ymap) {
+  auto kern = ecr_smallc2_kernel<C, FAST, RELU, TMA>;
+  const int smem = sc2_smem_bytes(C, 64);
+  static std::once_flag attr_once[64];
+  cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once[ctx->device & 63], [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  CK(attr_err);
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  const long grid = std::min<long>((a.total_items + kSc2Warps - 1) / kSc2Warps,
+                                   long(std::max(1, per_sm)) * ctx->num_sms);
+  Sc2SlotTable& t = sc2_slots(ctx->device);
+  std::lock_guard<std::mutex> lock(t.mu);
+  if (!t.base) CK(cudaGetSymbolAddress(reinterpret_cast<void**>(&t.base), c_sc2_w));
+  for (int kb = 0; kb < a.Kp / 64; ++kb) {
+    const int slot = t.next;
+    t.next = (t.next + 1) % kSc2Slots;
+    if (t.ev[slot]) CK(cudaStreamWaitEvent(cs, t.ev[slot], 0));
+    else CK(cudaEventCreateWithFlags(&t.ev[slot], cudaEventDisableTiming));
+    CK(cudaMemcpy2DAsync(t.base + size_t(slot) * kSc2SlotFloats, 64 * sizeof(float), wt + kb * 64,
+                         size_t(a.Kp) * sizeof(float), 64 * sizeof(float), size_t(C) * 9,
+                         cudaMemcpyDeviceToDevice, cs));
+    a.slot = slot;
+    a.k0 = kb * 64;
+    kern<<<static_cast<unsigned>(grid), 256, smem, cs>>>(a, ymap);
+    TRY(finish_launch(ctx, "ecr_smallc2_kernel"));
+    CK(cudaEventRecord(t.ev[slot], cs));
+  }
+  return SCONV_OK;
+}
+
+template <int C, bool FAST>
+int launch_smallc2_t(sconv_cu_ctx* ctx, cudaStream_t cs, const SmallC2Args& a, const float* wt) {
+  // outputs by TMA store when the row pitch allows a tensor map (OW % 4 == 0)
+  CUtensorMap ymap;
+  std::memset(&ymap, 0, sizeof(ymap));
+  bool tma = a.OW % 4 == 0 && !std::getenv("SCONV_SC2_STG");
+  if (tma) {
+    const CUresult r = encode_output_map(a.y, a.N, a.K, a.OH, a.OW, 32, kSc2Rows, kSc2KG, &ymap);
+    tma = r == CUDA_SUCCESS;
+  }
+  if (tma) return a.relu ? launch_smallc2_c<C, FAST, true, true>(ctx, cs, a, wt, ymap)
+                         : launch_smallc2_c<C, FAST, false, true>(ctx, cs, a, wt, ymap);
+  return a.relu ? launch_smallc2_c<C, FAST, true, false>(ctx, cs, a, wt, ymap)
+                : launch_smallc2_c<C, FAST, false, false>(ctx, cs, a, wt, ymap);
+}
+
+int launch_smallc2(sconv_cu_ctx* ctx, cudaStream_t cs, const float* dx, const float* wt, float* dy,
+                   int nb, int c, int h, int w, int k, int Kp, int OH, int OW, int relu, bool fast) {
+  const int bands = (OH + kSc2Rows - 1) / kSc2Rows, strips = (OW + 31) / 32;
+  if (nb == 0 || bands == 0 || strips == 0) return SCONV_OK;
+  // the kernel splits (item, filter group) units with 32-bit arithmetic
+  const int per = std::max(1, static_cast<int>(std::min<long>(nb, (1L << 26) / (long(bands) * strips))));
+  for (int n0 = 0; n0 < nb; n0 += per) {
+    const int m = std::min(per, nb - n0);
+    SmallC2Args a{dx + size_t(n0) * c * h * w, wt, dy + size_t(n0) * k * OH * OW, m, c, h, w, k, Kp,
+                  OH, OW, bands, strips, m * bands * strips, relu, 0, 0};
+    int rc = SCONV_OK;
+    switch (c * 2 + (fast ? 1 : 0)) {
+      case 2: rc = launch_smallc2_t<1, false>(ctx, cs, a, wt); break;
+      case 3: rc = launch_smallc2_t<1, true>(ctx, cs, a, wt); break;
+      case 4: rc = launch_smallc2_t<2, false>(ctx, cs, a, wt); break;
+      case 5: rc = launch_smallc2_t<2, true>(ctx, cs, a, wt); break;
+      case 6: rc = launch_smallc2_t<3, false>(ctx, cs, a, wt); break;
+      case 7: rc = launch_smallc2_t<3, true>(ctx, cs, a, wt); break;
+      case 8: rc = launch_smallc2_t<4, false>(ctx, cs, a, wt); break;
+      case 9: rc = launch_smallc2_t<4, true>(ctx, cs, a, wt); break;
+      default: return fail(ctx, SCONV_ERR_ARG, "small-C kernel: C = %d", c);
+    }
+    TRY(rc);
+  }
+  return SCONV_OK;
+}
+
 // One kernel launch over images [0, nb) of a chunk (device buffers).
 int launch_chunk(sconv_cu_ctx* ctx, const KernelChoice& ch, cudaStream_t cs, const float* dx,
                  const float* dw, const float* wt, float* dconv, float* dy, int nb, int c, int h,
                  int w, int k, int Kp, int kh, int kw, int stride, int OH, int OW, int pw, int ph,
                  int ps, int mode, int PHo, int PWo, bool pecr, bool fast) {
   const int model = ch.pool_after ? 0 : mode;
-  if (ch.smallc) {
+  cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+  if (ch.sc2) CK(cudaStreamIsCapturing(cs, &capturing));
+  if (ch.sc2 && capturing == cudaStreamCaptureStatusNone) {
+    TRY(launch_smallc2(ctx, cs, dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, model, fast));
+  } else if (ch.smallc) {
     SmallCArgs a{dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, model};
     if (ch.P < 0) {  // tiles of whole pool windows
       const int pth = (4 - ph) / ps + 1, ptw = (4 - pw) / ps + 1;
@@ -858,7 +966,17 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
                     pool_stride, flags, &ch));
   const bool smallc = ch.smallc;
   const int ws = ch.ws, which = ch.which;
-  if (smallc) {
+  if (ch.sc2) {  // persistent: grid = resident CTAs (at most one warp per item)
+    const long items = long(n) * ((OH + kSc2Rows - 1) / kSc2Rows) * ((OW + 31) / 32);
+    out->kernel = 301;
+    out->grid_x = static_cast<int>(std::min<long>((items + kSc2Warps - 1) / kSc2Warps, 2L * 148));
+    out->grid_y = out->grid_z = 1;
+    out->block_threads = 256;
+    out->smem_bytes = sc2_smem_bytes(c, (k + 63) / 64 * 64);
+    out->tile_h = kSc2Rows;
+    out->tile_w = 32;
+    out->tile_k = 64;
+  } else if (smallc) {
     const long tiles = long(n) * smallc_tiles(ch, OH, OW, pool_w, pool_h, pool_stride);
     out->kernel = 300;
     out->grid_x = static_cast<int>((tiles + 7) / 8);

@@ -505,11 +505,14 @@ def test_smallc(sc, orc, shape):
     n, c, h, w, k, sp = shape
     x, f = inputs(orc, n, c, h, w, k, 3, 3, sp, seed=(hash(shape) ^ 33) & 0xFFFF)
     ref, rops = orc.ecr_conv(x, f, 1)
-    assert sc.launch_plan(n, c, h, w, k, 3, 3, 1)["kernel"] == 300
+    # plain ECR: the lanes-over-pixels kernel (301); forced 'M' the per-tile one (300)
+    assert sc.launch_plan(n, c, h, w, k, 3, 3, 1)["kernel"] == 301
     ops = sc.OpCount()
     assert bits_equal(sc.ecr_conv_batched(x, f, 1, counters=ops), ref)
     assert (ops.multiplications, ops.additions) == rops
     assert close(sc.ecr_conv_batched(x, f, 1, fast=True), ref)
+    assert bits_equal(sc.ecr_conv_batched(x, f, 1, kernel="M"), ref)
+    assert close(sc.ecr_conv_batched(x, f, 1, fast=True, kernel="M"), ref)
     if (h - 2) % 2 == 0 and (w - 2) % 2 == 0:
         for mode in (0, 1):
             pref, _ = orc.pecr_conv(x, f, 1, 2, 2, 2, mode)
@@ -519,6 +522,29 @@ def test_smallc(sc, orc, shape):
     # forced on a wider map ('M')
     x2, f2 = inputs(orc, 1, 9, 12, 12, 64, 3, 3, 0.6, seed=5)
     assert bits_equal(sc.ecr_conv_batched(x2, f2, 1, kernel="M"), orc.ecr_conv(x2, f2, 1)[0])
+
+
+def test_smallc_nonfinite_weights(sc, orc):
+    """A zero cell drops out of the sum (ecr_convert keeps only v != 0,
+    src/ecr.cpp:84), so an Inf / NaN weight must not reach the outputs whose
+    window has a zero there.  The lanes-over-pixels kernel multiplies zero
+    cells when every weight is finite and predicates them off otherwise."""
+    x, f = inputs(orc, 2, 3, 20, 38, 64, 3, 3, 0.7, seed=91)
+    f = f.copy()
+    f[3, 1, 1, 1] = np.inf
+    f[10, 0, 0, 2] = -np.inf
+    f[17, 2, 2, 0] = np.nan
+    ref, _ = orc.ecr_conv(x, f, 1)
+    for fast in (False, True):
+        got = sc.ecr_conv_batched(x, f, 1, fast=fast)
+        fin = np.isfinite(ref)
+        assert np.array_equal(np.isnan(got), np.isnan(ref))
+        assert np.array_equal(got[~fin & ~np.isnan(ref)], ref[~fin & ~np.isnan(ref)])
+        if fast:
+            assert close(got[fin], ref[fin])
+        else:  # NaN payloads may differ between x86 and the GPU; every other value is bit-exact
+            nn = ~np.isnan(ref)
+            assert bits_equal(got[nn], ref[nn])
 
 
 @pytest.mark.slow

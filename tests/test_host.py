@@ -109,9 +109,14 @@ def test_shard_partition(sc):
 
 
 def test_launch_plan(sc):
-    # few input channels (conv1_1): the per-warp small-C kernel, 8 4x4 tiles per CTA
+    # few input channels (conv1_1): the persistent lanes-over-pixels kernel,
+    # work items of 4 rows x 32 columns, one CTA per resident slot
     p = sc.launch_plan(64, 3, 226, 226, 64, 3, 3, 1)
-    assert p["kernel"] == 300 and p["grid_x"] == 64 * 56 * 56 // 8 and p["block_threads"] == 256
+    assert p["kernel"] == 301 and p["grid_x"] == 2 * 148 and p["block_threads"] == 256
+    assert (p["tile_h"], p["tile_w"], p["tile_k"]) == (4, 32, 64)
+    # ... and the per-tile one for PECR
+    p = sc.launch_plan(64, 3, 226, 226, 64, 3, 3, 1, sc.PoolConfig(2, 2, 2))
+    assert p["kernel"] == 300 and p["grid_x"] == 64 * 56 * 56 // 8
     # K = 64: v3 with 6x6 tiles (WsG)
     p = sc.launch_plan(64, 64, 226, 226, 64, 3, 3, 1, sc.PoolConfig(2, 2, 2))
     assert p["kernel"] == 107 and p["smem_bytes"] <= 227 * 1024
