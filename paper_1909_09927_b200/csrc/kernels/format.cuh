@@ -177,15 +177,6 @@ __global__ void pecr_export_kernel(const PecrFmtArgs a) {
   if (PHASE == 0 && lane == 0) a.count[item] = filled;
 }
 
-// per-pack totals for the exclusive scan
-__global__ void pecr_pack_totals_kernel(const int32_t* count, int wpp, int npacks, int64_t* tot) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= npacks) return;
-  int64_t s = 0;
-  for (int n = 0; n < wpp; ++n) s += count[static_cast<size_t>(p) * wpp + n];
-  tot[p] = s;
-}
-
 // ---- PECR pooling over a format: pecr_conv_pool (src/pecr.cpp:133-172) ----
 struct PecrPoolArgs {
   const int32_t* count;

@@ -6,7 +6,6 @@
 // replaces plan()/dispatch() (src/exec.cpp:8-36, include/sconv/exec.hpp:57-120)
 // for the ECR / PECR entry points.
 #include <cuda_runtime.h>
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstdarg>
@@ -24,6 +23,7 @@
 #include "kernels/ingest.cuh"
 #include "kernels/smallc.cuh"
 #include "kernels/smallc2.cuh"
+#include "kernels/scan.cuh"
 #include "host/tma.h"
 
 using namespace sconv_cu;
@@ -1464,14 +1464,12 @@ int sconv_cu_pecr_count(sconv_cu_ctx* ctx, const float* x, int c, int h, int w, 
   const bool dev = flags & SCONV_F_DEVICE;
   const int wpp = pool_w * pool_h, npacks = PHo * PWo;
   DeviceGuard guard(ctx->device);
-  size_t scan_bytes = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, static_cast<int64_t*>(nullptr),
-                                static_cast<int64_t*>(nullptr), npacks);
+  const int64_t nparts = (int64_t(npacks) + kScanChunk - 1) / kScanChunk;
   Arena ar{ctx, {}};
   const size_t ix = dev ? 0 : ar.add(size_t(c) * h * w * 4);
   const size_t ic = dev ? 0 : ar.add(size_t(npacks) * wpp * 4);
   const size_t is = dev ? 0 : ar.add(size_t(npacks + 1) * 8);
-  const size_t it = ar.add(size_t(npacks) * 8), iscan = ar.add(scan_bytes + 16);
+  const size_t ipart = ar.add(size_t(std::max<int64_t>(nparts, 1)) * 8);
   std::vector<char*> p;
   TRY(ar.commit(p));
   cudaStream_t st = ctx->stream;
@@ -1486,12 +1484,18 @@ int sconv_cu_pecr_count(sconv_cu_ctx* ctx, const float* x, int c, int h, int w, 
   }
   pecr_export_kernel<0><<<grid_for(size_t(npacks) * wpp * 32, 256, 1 << 20), 256, 0, st>>>(a);
   TRY(finish_launch(ctx, "pecr_export_kernel<count>"));
-  int64_t* tot = reinterpret_cast<int64_t*>(p[it]);
-  pecr_pack_totals_kernel<<<(npacks + 255) / 256, 256, 0, st>>>(a.count, wpp, npacks, tot);
-  TRY(finish_launch(ctx, "pecr_pack_totals_kernel"));
-  CK(cudaMemsetAsync(dstart, 0, 8, st));
-  CK(cub::DeviceScan::InclusiveSum(p[iscan], scan_bytes, tot, dstart + 1, npacks, st));
-  ctx->launches++;
+  // pack_start = exclusive prefix of the pack totals (kernels/scan.cuh)
+  int64_t* part = reinterpret_cast<int64_t*>(p[ipart]);
+  if (npacks == 0) {
+    CK(cudaMemsetAsync(dstart, 0, 8, st));
+  } else {
+    pack_scan_partial<<<static_cast<unsigned>(nparts), kScanThreads, 0, st>>>(a.count, wpp, npacks, part);
+    TRY(finish_launch(ctx, "pack_scan_partial"));
+    pack_scan_partials<<<1, 1024, 0, st>>>(part, nparts);
+    TRY(finish_launch(ctx, "pack_scan_partials"));
+    pack_scan_final<<<static_cast<unsigned>(nparts), kScanThreads, 0, st>>>(a.count, wpp, npacks, part, dstart);
+    TRY(finish_launch(ctx, "pack_scan_final"));
+  }
   int64_t htotal = 0;
   CK(cudaMemcpyAsync(&htotal, dstart + npacks, 8, cudaMemcpyDeviceToHost, st));
   if (!dev) {

@@ -95,3 +95,57 @@ def test_cuda_hpp_batched_entries():
     r = _run("cuda_hpp_test")
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "cuda_hpp_test: ok" in r.stdout
+
+
+def _backend(args, env=None, timeout=600):
+    path = os.path.join(BUILD, "sparseconv")
+    if not os.path.exists(path):
+        pytest.skip("sparseconv not built (needs the reference mount; see tests/dropin/Makefile)")
+    e = dict(os.environ, **(env or {}))
+    return subprocess.run([path] + args, capture_output=True, text=True, timeout=timeout, env=e)
+
+
+def _checksum(out):
+    m = re.search(r"checksum=([0-9a-f]{16})", out)
+    return m.group(1) if m else None
+
+
+def test_cli_backend_switch_cpu(tmp_path):
+    """`sparseconv --backend cpu` is the unmodified reference CLI; an unknown
+    backend is a configuration error (exit 2)."""
+    m, k = str(tmp_path / "m.fmap"), str(tmp_path / "k.fmap")
+    assert _backend(["--backend", "cpu", "gen", "--height", "20", "--width", "20", "--channels", "8",
+                     "--sparsity", "0.7", "--seed", "3", "--out", m]).returncode == 0
+    assert _backend(["gen", "--backend=cpu", "--height", "3", "--width", "3", "--channels", "8",
+                     "--sparsity", "0", "--seed", "4", "--out", k]).returncode == 0
+    r = _backend(["--backend", "cpu", "conv", "--input", m, "--kernel", k])
+    assert r.returncode == 0 and _checksum(r.stdout)
+    bad = _backend(["--backend", "tpu", "conv", "--input", m, "--kernel", k])
+    assert bad.returncode == 2 and "unknown backend" in bad.stderr
+    assert _backend(["conv", "--backend"]).returncode == 2
+
+
+@pytest.mark.gpu
+def test_cli_backend_switch_cuda_vgg_layer(tmp_path):
+    """conv and convpool through `--backend cuda` (the drop-in, EXACT) on a
+    VGG-19 conv5-shaped layer (512 channels, 16x16 map, one filter, s = 0.7):
+    the same output checksum, op counts and exit code as `--backend cpu`; the
+    wall times of both land in the report (RunReport wall_ns)."""
+    m, k = str(tmp_path / "m.fmap"), str(tmp_path / "k.fmap")
+    assert _backend(["--backend", "cpu", "gen", "--height", "16", "--width", "16", "--channels", "512",
+                     "--sparsity", "0.7", "--seed", "51", "--out", m]).returncode == 0
+    assert _backend(["--backend", "cpu", "gen", "--height", "3", "--width", "3", "--channels", "512",
+                     "--sparsity", "0", "--seed", "52", "--out", k]).returncode == 0
+    env = {"SCONV_CUDA_MODE": "exact"}
+    for cmd in (["conv", "--method", "ecr"], ["convpool", "--method", "pecr", "--pool-h", "2",
+                                               "--pool-w", "2", "--pool-stride", "2"]):
+        outs = {}
+        for be in ("cpu", "cuda"):
+            rep = str(tmp_path / f"{cmd[0]}_{be}.json")
+            r = _backend(["--backend", be] + cmd + ["--input", m, "--kernel", k, "--report", rep], env)
+            assert r.returncode == 0, r.stderr
+            import json
+            with open(rep) as f:
+                outs[be] = json.load(f)
+        assert outs["cpu"]["output_checksum"] == outs["cuda"]["output_checksum"]
+        assert outs["cpu"]["op_count"] == outs["cuda"]["op_count"]
