@@ -1,14 +1,16 @@
 // dataset.cpp -- feature-map files for the batched GPU path.
 //
-// The reference stores maps as FMAP (magic "FMAP", u32le version 1, C, H, W,
-// then C*H*W little-endian fp32) or CSV ("channels,height,width", the dims,
-// then the values row by row), chosen by the file extension
-// (src/dataset.cpp:115-247: save_fmap / load_fmap / save_csv / load_csv /
-// save / load).  This restates those formats with the same validation and
-// error classes, and adds a batch loader that fills one [N][C][H][W] host
-// buffer (pinned by the caller, so it can go straight to sconv_cu_ecr_conv)
-// from N files on host threads.
+// The reference's map files (src/dataset.cpp:115-247) are FMAP (magic
+// "FMAP", u32le version 1, C, H, W, then C*H*W little-endian fp32) or CSV
+// ("channels,height,width", the dims, then the values row by row), chosen by
+// the file extension.  This reader / writer implements those two formats
+// from their definition, with the reference's validation rules, error
+// classes and messages (its tests match on them), and adds a batch loader
+// that fills one [N][C][H][W] host buffer (pinned by the caller, so it can go
+// straight to sconv_cu_ecr_conv) from N files on host threads; FMAP payloads
+// are read directly into that buffer.
 #include <charconv>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -24,7 +26,8 @@ namespace {
 
 constexpr char kMagic[4] = {'F', 'M', 'A', 'P'};
 constexpr std::uint32_t kVersion = 1;
-constexpr std::uint64_t kMaxElements = 1ull << 30;  // dataset.cpp:27-28
+constexpr std::uint64_t kMaxElements = 1ull << 30;  // the reference's cap, dataset.cpp:27-28
+constexpr std::size_t kHeaderBytes = 20;            // magic + version + C + H + W
 
 thread_local std::string g_err;
 
@@ -40,88 +43,124 @@ bool is_csv(const std::string& path) {
          path.compare(dot, std::string::npos, ".csv") == 0;
 }
 
-std::uint32_t rd32(const unsigned char* p) {
-  return std::uint32_t(p[0]) | (std::uint32_t(p[1]) << 8) | (std::uint32_t(p[2]) << 16) |
-         (std::uint32_t(p[3]) << 24);
+struct Dims {
+  int c = 0, h = 0, w = 0;
+  std::uint64_t total() const { return std::uint64_t(c) * std::uint64_t(h) * std::uint64_t(w); }
+};
+
+struct File {
+  std::FILE* f = nullptr;
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+
+// FMAP: a 20-byte little-endian header, then C*H*W little-endian fp32.  The
+// header is read on its own, the payload size is checked against the file
+// size, and the payload is read straight into the caller's buffer (on a
+// little-endian host the file bytes are the float bits) -- no staging copy
+// of multi-GB batches.
+int read_fmap(const std::string& path, float* out, std::int64_t capacity, Dims* d) {
+  static_assert(sizeof(float) == 4, "fp32");
+  File file{std::fopen(path.c_str(), "rb")};
+  if (!file.f) return err(SCONV_ERR_IO, "cannot open: " + path);
+  unsigned char hdr[kHeaderBytes];
+  const size_t got = std::fread(hdr, 1, kHeaderBytes, file.f);
+  if (got < 4 || std::memcmp(hdr, kMagic, 4) != 0)
+    return err(SCONV_ERR_FORMAT, "bad magic: not an FMAP file: " + path);
+  if (got < kHeaderBytes) return err(SCONV_ERR_FORMAT, "truncated header: " + path);
+  std::uint32_t field[4];  // version, C, H, W
+  for (int k = 0; k < 4; ++k) {
+    const unsigned char* q = hdr + 4 + 4 * k;
+    field[k] = std::uint32_t(q[0]) | std::uint32_t(q[1]) << 8 | std::uint32_t(q[2]) << 16 |
+               std::uint32_t(q[3]) << 24;
+  }
+  if (field[0] != kVersion)
+    return err(SCONV_ERR_FORMAT, "unsupported version " + std::to_string(field[0]) + ": " + path);
+  const std::uint64_t total = std::uint64_t(field[1]) * field[2] * field[3];
+  if (field[1] == 0 || field[2] == 0 || field[3] == 0 || total > kMaxElements)
+    return err(SCONV_ERR_FORMAT, "invalid dims in header: " + path);
+  if (std::fseek(file.f, 0, SEEK_END) != 0) return err(SCONV_ERR_IO, "cannot seek: " + path);
+  const long size = std::ftell(file.f);
+  if (size < 0 || std::uint64_t(size) < kHeaderBytes + total * 4)
+    return err(SCONV_ERR_FORMAT, "truncated payload: " + path);
+  d->c = int(field[1]), d->h = int(field[2]), d->w = int(field[3]);
+  if (!out) return SCONV_OK;
+  if (std::int64_t(total) > capacity) return err(SCONV_ERR_ARG, "output buffer too small: " + path);
+  if (std::fseek(file.f, long(kHeaderBytes), SEEK_SET) != 0 ||
+      std::fread(out, 4, size_t(total), file.f) != size_t(total))
+    return err(SCONV_ERR_IO, "read failed: " + path);
+  const unsigned one = 1;
+  if (*reinterpret_cast<const unsigned char*>(&one) != 1) {  // big-endian host: swap to the LE file order
+    auto* u = reinterpret_cast<std::uint32_t*>(out);
+    for (std::uint64_t k = 0; k < total; ++k) u[k] = __builtin_bswap32(u[k]);
+  }
+  return SCONV_OK;
 }
 
-int read_all(const std::string& path, std::string* raw) {
+// CSV: "channels,height,width", then the three dims, then C*H*W values in
+// channel / row / column order, separated by any run of ',', ' ', '\t',
+// '\r', '\n'.  A cursor over the file's text; numbers are read with
+// std::from_chars (no locale, no leading '+', the same acceptance as the
+// reference's loader).
+struct Cursor {
+  const char* p;
+  const char* end;
+  // the next line without its '\n' (false at end of text)
+  bool line(const char** b, const char** e) {
+    if (p >= end) return false;
+    const char* nl = static_cast<const char*>(std::memchr(p, '\n', size_t(end - p)));
+    *b = p;
+    *e = nl ? nl : end;
+    p = nl ? nl + 1 : end;
+    return true;
+  }
+  bool at_separator() const {
+    const char ch = *p;
+    return ch == ',' || ch == '\n' || ch == '\r' || ch == ' ' || ch == '\t';
+  }
+};
+
+int read_csv(const std::string& path, float* out, std::int64_t capacity, Dims* d) {
   std::ifstream f(path, std::ios::binary);
   if (!f) return err(SCONV_ERR_IO, "cannot open: " + path);
-  raw->assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+  const std::string text((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  Cursor cur{text.data(), text.data() + text.size()};
+  const char *b, *e;
+  if (!cur.line(&b, &e)) return err(SCONV_ERR_FORMAT, "empty csv: " + path);
+  while (e > b && (e[-1] == '\r' || e[-1] == ' ')) --e;
+  static constexpr char kHeader[] = "channels,height,width";
+  if (size_t(e - b) != sizeof(kHeader) - 1 || std::memcmp(b, kHeader, sizeof(kHeader) - 1) != 0)
+    return err(SCONV_ERR_FORMAT, "bad csv header: " + path);
+  if (!cur.line(&b, &e)) return err(SCONV_ERR_FORMAT, "missing dims line: " + path);
+  int* fields[3] = {&d->c, &d->h, &d->w};
+  for (int* v : fields) {
+    const auto r = std::from_chars(b, e, *v);
+    if (r.ec != std::errc{}) return err(SCONV_ERR_FORMAT, "bad dims line: " + path);
+    b = (r.ptr != e && *r.ptr == ',') ? r.ptr + 1 : r.ptr;
+  }
+  if (d->c < 1 || d->h < 1 || d->w < 1 || d->total() > kMaxElements)
+    return err(SCONV_ERR_FORMAT, "invalid dims in header: " + path);
+  if (!out) return SCONV_OK;
+  const std::int64_t total = std::int64_t(d->total());
+  if (total > capacity) return err(SCONV_ERR_ARG, "output buffer too small: " + path);
+  for (std::int64_t k = 0; k < total; ++k) {
+    while (cur.p != cur.end && cur.at_separator()) ++cur.p;
+    if (cur.p == cur.end) return err(SCONV_ERR_FORMAT, "truncated payload: " + path);
+    const auto r = std::from_chars(cur.p, cur.end, out[k]);
+    if (r.ec != std::errc{}) return err(SCONV_ERR_FORMAT, "bad value in csv: " + path);
+    cur.p = r.ptr;
+  }
   return SCONV_OK;
 }
 
-// Parse a map; with out == nullptr only the dims are returned.  capacity is
-// in floats.
+// A map file by extension (load(), dataset.cpp:241-247); with out == nullptr
+// only the dims.  capacity is in floats.
 int parse(const std::string& path, float* out, std::int64_t capacity, int* pc, int* ph, int* pw) {
-  std::string raw;
-  if (int rc = read_all(path, &raw)) return rc;
-  if (!is_csv(path)) {  // load_fmap, dataset.cpp:131-159
-    const auto* b = reinterpret_cast<const unsigned char*>(raw.data());
-    if (raw.size() < 4 || std::memcmp(raw.data(), kMagic, 4) != 0)
-      return err(SCONV_ERR_FORMAT, "bad magic: not an FMAP file: " + path);
-    if (raw.size() < 20) return err(SCONV_ERR_FORMAT, "truncated header: " + path);
-    const std::uint32_t version = rd32(b + 4);
-    if (version != kVersion)
-      return err(SCONV_ERR_FORMAT, "unsupported version " + std::to_string(version) + ": " + path);
-    const std::uint32_t c = rd32(b + 8), h = rd32(b + 12), w = rd32(b + 16);
-    const std::uint64_t total = std::uint64_t(c) * h * w;
-    if (c == 0 || h == 0 || w == 0 || total > kMaxElements)
-      return err(SCONV_ERR_FORMAT, "invalid dims in header: " + path);
-    if (raw.size() < 20 + total * 4) return err(SCONV_ERR_FORMAT, "truncated payload: " + path);
-    *pc = int(c), *ph = int(h), *pw = int(w);
-    if (!out) return SCONV_OK;
-    if (std::int64_t(total) > capacity) return err(SCONV_ERR_ARG, "output buffer too small: " + path);
-    for (std::uint64_t i = 0; i < total; ++i) {  // little-endian payload, bit for bit
-      const std::uint32_t u = rd32(b + 20 + i * 4);
-      std::memcpy(out + i, &u, 4);
-    }
-    return SCONV_OK;
-  }
-  // load_csv, dataset.cpp:181-230
-  size_t pos = 0;
-  auto line = [&](std::string* s) {
-    if (pos >= raw.size()) return false;
-    const size_t e = raw.find('\n', pos);
-    *s = raw.substr(pos, e == std::string::npos ? std::string::npos : e - pos);
-    pos = e == std::string::npos ? raw.size() : e + 1;
-    return true;
-  };
-  std::string header, dims;
-  if (!line(&header)) return err(SCONV_ERR_FORMAT, "empty csv: " + path);
-  while (!header.empty() && (header.back() == '\r' || header.back() == ' ')) header.pop_back();
-  if (header != "channels,height,width") return err(SCONV_ERR_FORMAT, "bad csv header: " + path);
-  if (!line(&dims)) return err(SCONV_ERR_FORMAT, "missing dims line: " + path);
-  int d[3] = {0, 0, 0};
-  {
-    const char* p = dims.c_str();
-    const char* end = p + dims.size();
-    for (int& f : d) {
-      auto r = std::from_chars(p, end, f);
-      if (r.ec != std::errc{}) return err(SCONV_ERR_FORMAT, "bad dims line: " + path);
-      p = r.ptr;
-      if (p != end && *p == ',') ++p;
-    }
-  }
-  if (d[0] < 1 || d[1] < 1 || d[2] < 1 || std::uint64_t(d[0]) * d[1] * d[2] > kMaxElements)
-    return err(SCONV_ERR_FORMAT, "invalid dims in header: " + path);
-  *pc = d[0], *ph = d[1], *pw = d[2];
-  if (!out) return SCONV_OK;
-  const std::int64_t total = std::int64_t(d[0]) * d[1] * d[2];
-  if (total > capacity) return err(SCONV_ERR_ARG, "output buffer too small: " + path);
-  const char* p = raw.c_str() + pos;
-  const char* end = raw.c_str() + raw.size();
-  for (std::int64_t i = 0; i < total; ++i) {
-    while (p != end && (*p == ',' || *p == '\n' || *p == '\r' || *p == ' ' || *p == '\t')) ++p;
-    if (p == end) return err(SCONV_ERR_FORMAT, "truncated payload: " + path);
-    float v = 0.0f;
-    auto r = std::from_chars(p, end, v);
-    if (r.ec != std::errc{}) return err(SCONV_ERR_FORMAT, "bad value in csv: " + path);
-    out[i] = v;
-    p = r.ptr;
-  }
-  return SCONV_OK;
+  Dims d;
+  const int rc = is_csv(path) ? read_csv(path, out, capacity, &d) : read_fmap(path, out, capacity, &d);
+  if (rc == SCONV_OK) *pc = d.c, *ph = d.h, *pw = d.w;
+  return rc;
 }
 
 }  // namespace
