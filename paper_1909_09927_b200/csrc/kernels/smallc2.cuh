@@ -77,10 +77,15 @@ __constant__ float4 c_sc2_w[kSc2Slots][kSc2SlotFloats / 4];
 constexpr int kSc2Rows = 4;                       // output rows per work item
 constexpr int kSc2KG = SCONV_SC2_KG;              // filters per pass of a lane
 constexpr int kSc2WinRows = kSc2Rows + 2;         // input rows of its window
-constexpr int kSc2Pitch = 36;                     // window row pitch (floats)
+#ifndef SCONV_SC2_SPLIT  // TMA store boxes per filter group (1: one KG-filter box; 2: two halves)
+#define SCONV_SC2_SPLIT 2
+#endif
+constexpr int kSc2Pitch = 34;                     // window row pitch (floats)
 constexpr int kSc2Chan = kSc2WinRows * kSc2Pitch; // one channel of a window
 
-constexpr int kSc2Out = kSc2KG * kSc2Rows * 32;  // one warp's output box (floats)
+constexpr int kSc2Split = SCONV_SC2_SPLIT;
+constexpr int kSc2BoxK = kSc2KG / kSc2Split;      // filters per TMA store box
+constexpr int kSc2Out = kSc2BoxK * kSc2Rows * 32; // one warp's staging slot (floats)
 
 __host__ __device__ constexpr int sc2_smem_bytes(int C, int Kp) {
   return (2 * kSc2Warps * C * kSc2Chan + kSc2Warps * kSc2Out) * 4;
@@ -233,25 +238,33 @@ __global__ void __launch_bounds__(256, SCONV_SC2_MINB)
         sc2_terms<C, FAST, true>(acc, wn, wk + (kSc2KG / 4) * g);
       }
       if constexpr (TMA) {
-        // the warp's KG x 4 x 32 box goes out by one TMA store (rows past
-        // OH, columns past OW and filters past K are clipped by the unit);
-        // its staging slot is free once the previous store has read it
+        // the warp's KG x 4 x 32 outputs go out as kSc2Split TMA stores of
+        // BoxK filters (rows past OH, columns past OW and filters past K are
+        // clipped by the unit); the staging slot is refilled once the
+        // previous store has read it (2 KB slots: 4 CTAs fit an SM)
         float* ob = ost + warp * kSc2Out + lane;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncwarp();
+        const unsigned slot = static_cast<unsigned>(__cvta_generic_to_shared(ost + warp * kSc2Out));
 #pragma unroll
-        for (int k = 0; k < kSc2KG; ++k)
+        for (int hbox = 0; hbox < kSc2Split; ++hbox) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
 #pragma unroll
-          for (int r = 0; r < kSc2Rows; ++r) ob[(k * kSc2Rows + r) * 32] = RELU ? relu_f(acc[r][k]) : acc[r][k];
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          asm volatile(
-              "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
-              ::"l"(reinterpret_cast<uint64_t>(&ymap)), "r"(x0), "r"(y0), "r"(a.k0 + kSc2KG * g),
-                "r"(n), "r"(static_cast<unsigned>(__cvta_generic_to_shared(ost + warp * kSc2Out)))
-              : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          for (int k = 0; k < kSc2BoxK; ++k)
+#pragma unroll
+            for (int r = 0; r < kSc2Rows; ++r) {
+              const float v = acc[r][hbox * kSc2BoxK + k];
+              ob[(k * kSc2Rows + r) * 32] = RELU ? relu_f(v) : v;
+            }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+                ::"l"(reinterpret_cast<uint64_t>(&ymap)), "r"(x0), "r"(y0),
+                  "r"(a.k0 + kSc2KG * g + hbox * kSc2BoxK), "r"(n), "r"(slot)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
         }
       } else if (col_ok) {
         // plain stores: each writes one 128-byte segment of one channel row

@@ -391,7 +391,7 @@ int launch_smallc2_t(sconv_cu_ctx* ctx, cudaStream_t cs, const SmallC2Args& a, c
   std::memset(&ymap, 0, sizeof(ymap));
   bool tma = a.OW % 4 == 0 && !std::getenv("SCONV_SC2_STG");
   if (tma) {
-    const CUresult r = encode_output_map(a.y, a.N, a.K, a.OH, a.OW, 32, kSc2Rows, kSc2KG, &ymap);
+    const CUresult r = encode_output_map(a.y, a.N, a.K, a.OH, a.OW, 32, kSc2Rows, kSc2BoxK, &ymap);
     tma = r == CUDA_SUCCESS;
   }
   if (tma) return a.relu ? launch_smallc2_c<C, FAST, true, true>(ctx, cs, a, wt, ymap)
