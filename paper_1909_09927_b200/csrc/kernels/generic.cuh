@@ -75,15 +75,30 @@ __global__ void pecr_generic_kernel(const GenericArgs a) {
 }
 
 // Filter re-layout for the tiled kernels: wt[c][i*kw+j][k] = w[k][c][i][j],
-// rows padded to Kp >= K output channels with zeros (16B-aligned rows).
-__global__ void transpose_filters_kernel(const float* __restrict__ w, float* __restrict__ wt, int K,
-                                         int Kp, int C, int KK) {
-  const size_t total = static_cast<size_t>(Kp) * C * KK;
-  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const int k = static_cast<int>(idx % Kp);
-    const size_t cij = idx / Kp;  // c*KK + ij
-    wt[idx] = k < K ? __ldg(w + static_cast<size_t>(k) * C * KK + cij) : 0.0f;
+// rows padded to Kp >= K output channels with zeros (16B-aligned rows).  A
+// transpose of the K x M matrix (M = C*kh*kw) through 32 x 33 shared tiles:
+// both the reads (along m) and the writes (along k) are coalesced.
+// grid = (ceil(Kp / 32), ceil(M / 32)), block = 32 x 8.
+__global__ void __launch_bounds__(256) transpose_filters_kernel(const float* __restrict__ w,
+                                                                float* __restrict__ wt, int K,
+                                                                int Kp, int C, int KK) {
+  __shared__ float tile[32][33];
+  const long long M = static_cast<long long>(C) * KK;
+  const int k0 = blockIdx.x * 32;
+  const long long m0 = static_cast<long long>(blockIdx.y) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {  // tile[k][m] = w[k0 + r][m0 + tx]
+    const int k = k0 + r;
+    const long long m = m0 + tx;
+    tile[r][tx] = (k < K && m < M) ? __ldg(w + static_cast<long long>(k) * M + m) : 0.0f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {  // wt[m0 + r][k0 + tx] = tile[tx][r]
+    const long long m = m0 + r;
+    const int k = k0 + tx;
+    if (m < M && k < Kp) wt[m * Kp + k] = tile[tx][r];
   }
 }
 

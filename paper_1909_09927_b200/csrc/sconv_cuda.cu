@@ -650,8 +650,8 @@ int fused_conv(sconv_cu_ctx* ctx, const float* x, int n, int c, int h, int w, co
     }
   }
   if (need_wt && (!fe || fresh)) {
-    transpose_filters_kernel<<<grid_for(size_t(Kp) * c * kh * kw, 256, ctx->num_sms), 256, 0, st>>>(
-        dw, const_cast<float*>(wt), k, Kp, c, kh * kw);
+    const dim3 tgrid((Kp + 31) / 32, static_cast<unsigned>((size_t(c) * kh * kw + 31) / 32));
+    transpose_filters_kernel<<<tgrid, dim3(32, 8), 0, st>>>(dw, const_cast<float*>(wt), k, Kp, c, kh * kw);
     TRY(finish_launch(ctx, "transpose_filters_kernel"));
   }
   if (counters) CK(cudaMemsetAsync(dops, 0, 16, st));
