@@ -71,8 +71,8 @@ constexpr int kSc2SlotFloats = 4 * 9 * 64;        // C <= 4 channels x 9 taps x 
 
 // The filters of one launch ([C][9][64], one K-block), read by every lane at
 // the same address: from the constant bank they feed FFMA2 as uniform
-// registers (LDCU.128, 16 bytes per warp), where a shared-memory broadcast
-// would return 512 bytes per warp through the LSU.
+// registers (one LDCU.64 per weight pair, 8 bytes per warp), where a
+// shared-memory broadcast would return 512 bytes per warp through the LSU.
 __constant__ float4 c_sc2_w[kSc2Slots][kSc2SlotFloats / 4];
 constexpr int kSc2Rows = 4;                       // output rows per work item
 constexpr int kSc2KG = SCONV_SC2_KG;              // filters per pass of a lane
@@ -102,11 +102,11 @@ __device__ __forceinline__ void mac2(float& a0, float& a1, float w0, float w1, f
   }
 }
 
-// The 9C terms of 4 output rows x 16 filters of one lane, in (c, i, j)
+// The 9C terms of 4 output rows x KG filters of one lane, in (c, i, j)
 // order: lane l's cell of term (c, i, j) for output row r is
-// win[c][r + i][l + j]; the 16 weights of the term (filters 16g .. 16g+15)
-// come from the constant bank as uniform registers, each pair feeding one
-// FFMA2 per output row.  A zero cell contributes nothing: with finite weights
+// win[c][r + i][l + j]; the KG weights of the term (filters KG*g ..
+// KG*g + KG-1) come from the constant bank as uniform registers, each pair
+// feeding one FFMA2 per output row.  A zero cell contributes nothing: with finite weights
 // its products are +-0 and acc + (+-0) == acc (acc is never -0: it starts at
 // +0 and a round-to-nearest sum is -0 only when both addends are), so the
 // FFMA2 run unconditionally; SKIP = true (some weight is Inf / NaN, whose
