@@ -74,7 +74,10 @@ constexpr int kSc2SlotFloats = 4 * 9 * 64;        // C <= 4 channels x 9 taps x 
 // registers (one LDCU.64 per weight pair, 8 bytes per warp), where a
 // shared-memory broadcast would return 512 bytes per warp through the LSU.
 __constant__ float4 c_sc2_w[kSc2Slots][kSc2SlotFloats / 4];
-constexpr int kSc2Rows = 4;                       // output rows per work item
+#ifndef SCONV_SC2_ROWS  // output rows per work item (and per lane)
+#define SCONV_SC2_ROWS 4
+#endif
+constexpr int kSc2Rows = SCONV_SC2_ROWS;
 constexpr int kSc2KG = SCONV_SC2_KG;              // filters per pass of a lane
 constexpr int kSc2WinRows = kSc2Rows + 2;         // input rows of its window
 #ifndef SCONV_SC2_SPLIT  // TMA store boxes per filter group (1: one KG-filter box; 2: two halves)
