@@ -688,3 +688,43 @@ def test_signed_zeros_and_negative_inputs(sc, orc, kid):
     ops = sc.OpCount()
     p = sc.pecr_conv_pool_batched(x, f, 1, pool, counters=ops, generic=generic, kernel=kernel)
     assert bits_equal(p, pref) and (ops.multiplications, ops.additions) == pops
+
+
+def test_smallc_concurrent_contexts(sc, orc):
+    """The small-C kernel keeps each launch's filters in one of 4 constant-memory
+    slots per device, copied on the launch's stream and released by an event.
+    Six host threads, each with its own context (own stream), run conv1_1-shaped
+    launches with different filters at the same time -- more launches in flight
+    than slots -- and every output must still be its own filters' result."""
+    import ctypes as C
+    import threading
+    from paper_1909_09927_b200 import _native as nat
+    L = nat.lib()
+    jobs = []
+    for t in range(6):
+        x, f = inputs(orc, 3, 3, 34, 66, 64, 3, 3, 0.7, seed=700 + t)
+        ref, _ = orc.ecr_conv(x, f, 1)
+        jobs.append((np.ascontiguousarray(x), np.ascontiguousarray(f), ref))
+    outs = [np.empty_like(j[2]) for j in jobs]
+    errs = []
+
+    def work(t):
+        try:
+            ctx = nat.Context(0)
+            x, f, _ = jobs[t]
+            for rep in range(4):
+                nat.check(L.sconv_cu_ecr_conv(ctx.handle, x.ctypes.data, 3, 3, 34, 66, f.ctypes.data,
+                                              64, 3, 3, 1, outs[t].ctypes.data, None, None,
+                                              nat.F_EXACT), ctx.handle)
+            ctx.close()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+    for h in th:
+        h.start()
+    for h in th:
+        h.join()
+    assert not errs, errs
+    for (x, f, ref), got in zip(jobs, outs):
+        assert bits_equal(got, ref)
