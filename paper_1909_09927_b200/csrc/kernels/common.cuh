@@ -36,6 +36,24 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float w0, float w1, 
       : "f"(w0), "f"(w1), "f"(v));
 }
 
+// Two EXACT terms, {a0,a1} += {w0,w1}*v as a rounded product then a rounded
+// sum per half -- the reference's `acc += a*b` without contraction
+// (src/ecr.cpp:117-120) -- in three issue slots instead of four: one packed
+// FMUL2 and two scalar FADDs.  (A packed mul.rn.f32x2 followed by a packed
+// add.rn.f32x2 is NOT used: ptxas 12.9 fuses that pair into an FFMA2 even
+// with -fmad=false, which would round once instead of twice.)
+__device__ __forceinline__ void exact2(float& a0, float& a1, float w0, float w1, float v) {
+  asm("{\n\t.reg .b64 w, v, t;\n\t.reg .f32 t0, t1;\n\t"
+      "mov.b64 w, {%2, %3};\n\t"
+      "mov.b64 v, {%4, %4};\n\t"
+      "mul.rn.f32x2 t, w, v;\n\t"
+      "mov.b64 {t0, t1}, t;\n\t"
+      "add.rn.f32 %0, %0, t0;\n\t"
+      "add.rn.f32 %1, %1, t1;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(w0), "f"(w1), "f"(v));
+}
+
 // Keeps ptxas from if-converting a zero-skip block into predicated FMAs
 // (which would issue -- and occupy the FMA pipe -- for every zero too).  It
 // emits one PMTRIG, which touches no registers; ptxas will not predicate a

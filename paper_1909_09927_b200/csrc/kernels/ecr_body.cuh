@@ -25,6 +25,11 @@
 
 #include "common.cuh"
 
+// EXACT arithmetic with packed f32x2 mul + add (1) or scalar FMUL + FADD (0)
+#ifndef SCONV_EXACT2
+#define SCONV_EXACT2 1
+#endif
+
 // 0: let ptxas if-convert small blocks; 2: keep every block behind its branch
 #ifndef SCONV_BODY_GUARD
 #define SCONV_BODY_GUARD 0
@@ -78,11 +83,16 @@ __device__ __forceinline__ void ecr_channel(float (&acc)[TH][TW][R], const float
           for (int j = 0; j < KW; ++j) {
             const int dx = X - j;
             if (dx < 0 || dx % S != 0 || dx / S >= TW) continue;
-            if constexpr (FAST && R % 2 == 0) {
+            if constexpr (R % 2 == 0 && (FAST || SCONV_EXACT2)) {
 #pragma unroll
-              for (int r = 0; r < R; r += 2)
-                ffma2(acc[dy / S][dx / S][r], acc[dy / S][dx / S][r + 1], wr[i * KW + j][r],
-                      wr[i * KW + j][r + 1], v);
+              for (int r = 0; r < R; r += 2) {
+                if constexpr (FAST)
+                  ffma2(acc[dy / S][dx / S][r], acc[dy / S][dx / S][r + 1], wr[i * KW + j][r],
+                        wr[i * KW + j][r + 1], v);
+                else
+                  exact2(acc[dy / S][dx / S][r], acc[dy / S][dx / S][r + 1], wr[i * KW + j][r],
+                         wr[i * KW + j][r + 1], v);
+              }
             } else {
 #pragma unroll
               for (int r = 0; r < R; ++r)

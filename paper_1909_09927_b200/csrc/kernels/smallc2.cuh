@@ -100,8 +100,7 @@ __device__ __forceinline__ void mac2(float& a0, float& a1, float w0, float w1, f
   if constexpr (FAST) {
     ffma2(a0, a1, w0, w1, v);
   } else {
-    a0 = __fadd_rn(a0, __fmul_rn(w0, v));
-    a1 = __fadd_rn(a1, __fmul_rn(w1, v));
+    exact2(a0, a1, w0, w1, v);
   }
 }
 
