@@ -12,6 +12,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -345,8 +347,12 @@ struct Sc2SlotTable {
   float* base = nullptr;  // device address of c_sc2_w (floats)
 };
 Sc2SlotTable& sc2_slots(int device) {
-  static Sc2SlotTable tables[64];
-  return tables[device & 63];
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<Sc2SlotTable>> tables;  // one per device
+  std::lock_guard<std::mutex> lock(mu);
+  std::unique_ptr<Sc2SlotTable>& t = tables[device];
+  if (!t) t.reset(new Sc2SlotTable);
+  return *t;
 }
 
 template <int C, bool FAST, bool RELU, bool TMA>
