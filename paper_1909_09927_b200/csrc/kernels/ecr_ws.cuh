@@ -39,7 +39,7 @@ namespace sconv_cu {
 #endif
 
 #ifndef SCONV_SPARSE_PCT_WIDE  // see WsCfg::SPARSE_PCT
-#define SCONV_SPARSE_PCT_WIDE 25
+#define SCONV_SPARSE_PCT_WIDE 100
 #endif
 
 template <int KH_, int KW_, int S_, int TH_, int TW_, int R_, int WPC_, int CC_, int NS_, int P_>
@@ -75,7 +75,11 @@ struct WsCfg {
   // border cells ptxas predicates (their FFMA2 run even for zero cells).
   // Measured (A/B, tools/gpu_ab2.sh): with R = 2 or 2-row tiles the border
   // cells carry so little work that branching always wins (conv5 2x7 -3.5%,
-  // conv1_2 ECR -2.3%); 4x4 R = 4 tiles prefer predication above 25%.
+  // conv1_2 ECR -2.3%).  4x4 R = 4 tiles preferred predication above 25% in
+  // round 1; re-measured on the round-2 build (tools/gpu_runs/gpu_r2_pct.sh)
+  // the fully branched body everywhere is 0.3-0.8% faster at s = 0.7 and
+  // equal at 0.9 (threshold 0: 1-4% slower at 0.7, 20-26% at 0.9), so WIDE
+  // is now 100 -- one body per channel, half the hot code.
   // 2x2 tiles and 1x1 windows are the opposite case: a cell feeds at most
   // four outputs (one for 1x1), so its one to eight FFMA2 cost less than the
   // branch that would skip it, and only all-zero windows branch.  Measured:
