@@ -79,7 +79,9 @@ struct WsCfg {
   // round 1; re-measured on the round-2 build (tools/gpu_runs/gpu_r2_pct.sh)
   // the fully branched body everywhere is 0.3-0.8% faster at s = 0.7 and
   // equal at 0.9 (threshold 0: 1-4% slower at 0.7, 20-26% at 0.9), so WIDE
-  // is now 100 -- one body per channel, half the hot code.
+  // is now 100 -- one body per channel, half the hot code.  (The dense body
+  // with every cell branched and no row tests: 0-2.5% slower at 0.7, 29% at
+  // 0.9.)
   // 2x2 tiles and 1x1 windows are the opposite case: a cell feeds at most
   // four outputs (one for 1x1), so its one to eight FFMA2 cost less than the
   // branch that would skip it, and only all-zero windows branch.  Measured:
