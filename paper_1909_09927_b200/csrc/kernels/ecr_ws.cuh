@@ -222,9 +222,13 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
   const int warp = __shfl_sync(kFull, tid >> 5, 0), lane = tid & 31;
   // K-blocks vary fastest over the linear grid, so the CTAs that read the same
   // input patches run together and the patch is fetched from HBM once.
+  // Work items (tile group x K-block), K-blocks fastest; a CTA takes items
+  // blockIdx.x, + gridDim.x, ... (one each unless the host launched a
+  // persistent grid: then the ring runs on across items -- the producer
+  // stages the next item's first chunks while the consumers store the last
+  // one's outputs -- and a CTA's fill and drain are paid once).
   const int kblocks = (a.K + KT - 1) / KT;
-  const int cta = blockIdx.x / kblocks;
-  const int k0 = (blockIdx.x - cta * kblocks) * KT;
+  const int items = (a.total_tiles + WPC - 1) / WPC * kblocks;
   const int C = a.C, H = a.H, W = a.W, K = a.K;
   const int nchunks = (C + CC - 1) / CC;
 
@@ -244,6 +248,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
       // warp-uniform: 8-byte aligned cell pairs (every window row starts on
       // an even column; general-pool tiles may step by an odd stride)
       if ((W & 1) == 0 && ((a.tsx * S) & 1) == 0) {
+        if (lane == 0)
+          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
+        for (int item = blockIdx.x, it = 0; item < items; item += gridDim.x, ++it) {
+        const int cta = item / kblocks, k0 = (item - cta * kblocks) * KT, kbase = it * nchunks;
         int src_off[Cfg::PAIRS_PER_LANE];
         int dst_off[Cfg::PAIRS_PER_LANE];
         int bytes[Cfg::PAIRS_PER_LANE];
@@ -261,11 +269,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
           src_off[e] = ok ? static_cast<int>((static_cast<size_t>(n) * C * H + iy) * W + ix) : 0;
           dst_off[e] = (wi * CC) * PATCH + Y * PITCH + X;
         }
-        if (lane == 0)
-          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
         for (int k = 0; k < nchunks; ++k) {
-          const int s = k % NS;
-          if (k >= NS) mbar_wait_sleep(&empty[s], ((k / NS) + 1) & 1);
+          const int kk = kbase + k, s = kk % NS;
+          if (kk >= NS) mbar_wait_sleep(&empty[s], ((kk / NS) + 1) & 1);
           float* in_s = smem + s * Cfg::STAGE;
           float* w_s = in_s + Cfg::IN_STAGE;
           const int c0 = k * CC;
@@ -286,10 +292,15 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
           }
           mbar_arrive_cp_async(&full[s]);
         }
+        }  // items
         cp_async_wait<0>();
         return;
       }
     }
+    if (lane == 0)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
+    for (int item = blockIdx.x, it = 0; item < items; item += gridDim.x, ++it) {
+    const int cta = item / kblocks, k0 = (item - cta * kblocks) * KT, kbase = it * nchunks;
     int src_off[Cfg::CELLS_PER_LANE];
     int dst_off[Cfg::CELLS_PER_LANE];
     bool ok[Cfg::CELLS_PER_LANE];
@@ -306,11 +317,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
       src_off[e] = ok[e] ? static_cast<int>((static_cast<size_t>(n) * C * H + iy) * W + ix) : 0;
       dst_off[e] = (wi * CC) * PATCH + Y * PITCH + X;
     }
-    if (lane == 0)
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
     for (int k = 0; k < nchunks; ++k) {
-      const int s = k % NS;
-      if (k >= NS) mbar_wait_sleep(&empty[s], ((k / NS) + 1) & 1);
+      const int kk = kbase + k, s = kk % NS;
+      if (kk >= NS) mbar_wait_sleep(&empty[s], ((kk / NS) + 1) & 1);
       float* in_s = smem + s * Cfg::STAGE;
       float* w_s = in_s + Cfg::IN_STAGE;
       const int c0 = k * CC;
@@ -331,11 +340,18 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
       }
       mbar_arrive_cp_async(&full[s]);
     }
+    }  // items
     cp_async_wait<0>();
     return;
   }
 
   // ------------------------------- consumers -------------------------------
+  // Lane l tests sub-patch cells l and l+32 (bit = Y*PITCH + X).
+  const bool t0 = (lane % PITCH) < WPW && (lane / PITCH) < WPH;
+  const bool t1 = ((lane + 32) % PITCH) < WPW && ((lane + 32) / PITCH) < WPH;
+  constexpr bool TWO = WPH * PITCH > 32;
+  for (int item = blockIdx.x, it = 0; item < items; item += gridDim.x, ++it) {
+  const int cta = item / kblocks, k0 = (item - cta * kblocks) * KT, kbase = it * nchunks;
   const int t = cta * WPC + warp;
   const bool active = t < a.total_tiles;
   const int n = active ? t / a.tiles_per_img : 0;
@@ -350,14 +366,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[i][j][r] = 0.0f;
 
-  // Lane l tests sub-patch cells l and l+32 (bit = Y*PITCH + X).
-  const bool t0 = (lane % PITCH) < WPW && (lane / PITCH) < WPH;
-  const bool t1 = ((lane + 32) % PITCH) < WPW && ((lane + 32) / PITCH) < WPH;
-  constexpr bool TWO = WPH * PITCH > 32;
-
   for (int k = 0; k < nchunks; ++k) {
-    const int s = k % NS;
-    mbar_wait(&full[s], (k / NS) & 1);
+    const int kk = kbase + k, s = kk % NS;
+    mbar_wait(&full[s], (kk / NS) & 1);
     if (active) {
       const float* ic = smem + s * Cfg::STAGE + warp * CC * PATCH;
       const float* wsrc = smem + s * Cfg::STAGE + Cfg::IN_STAGE;
@@ -397,7 +408,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
     // `full` wait of each consumer already observed
     asm volatile("bar.sync 1, %0;" ::"r"(WPC * 32) : "memory");
   }
-  if (!active) return;
+  if (!active) continue;
 
   // ---- epilogue ------------------------------------------------------------
   const int oy0 = ty * a.tsy, ox0 = tx * a.tsx;
@@ -480,6 +491,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
       }
     }
   }
+  }  // items
 }
 
 }  // namespace sconv_cu
