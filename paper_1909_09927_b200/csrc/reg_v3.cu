@@ -71,8 +71,11 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4, lon
   // 450 us) warp tiles.  With the 15-consumer CTA the 4x4 tiles also beat the
   // waste-free 2x7 tiles (WsB) on 14x14 maps at every batch measured (conv5_1
   // at 64: 797 vs 819 us; at 16: WsE 311 vs WsB 319 us), so WsB is forced-only.
-  // tiles4 = 4x4 output tiles x K-blocks of 128.
-  return (C >= 128 && tiles4 >= 148L * 10) ? 1 : 5;
+  // tiles4 = 4x4 output tiles x K-blocks of 128.  Round 2: with the
+  // persistent grid WsA runs for C <= 128 (reg_v3.inc), its ring no longer
+  // refills per CTA and it also wins at C = 64 (conv2_1 1254 vs WsE 1355 us,
+  // tools/gpu_runs/gpu_r2_c12.sh).
+  return (C >= 64 && tiles4 >= 148L * 10) ? 1 : 5;
 }
 
 // The general-pool config for a window / pool geometry (0 = none: the pool

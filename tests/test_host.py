@@ -125,8 +125,11 @@ def test_launch_plan(sc):
     p = sc.launch_plan(64, 512, 30, 30, 512, 3, 3, 1)
     assert p["kernel"] == 101 and p["grid_y"] == 1 and p["block_threads"] == 512
     assert p["grid_x"] == (64 * 7 * 7 + 14) // 15 * 4 and p["grid_z"] == 1
-    # C < 128: two CTAs of 7 consumers per SM (WsE)
+    # C = 64 (conv2_1), big grid: the 15-consumer CTA too (persistent for C <= 128)
     p = sc.launch_plan(64, 64, 114, 114, 128, 3, 3, 1)
+    assert p["kernel"] == 101 and p["block_threads"] == 512
+    # C < 64: two CTAs of 7 consumers per SM (WsE)
+    p = sc.launch_plan(64, 32, 114, 114, 128, 3, 3, 1)
     assert p["kernel"] == 105 and p["block_threads"] == 256
     p = sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1)  # 14x14 maps, big grid: 15-warp CTAs
     assert p["kernel"] == 101
