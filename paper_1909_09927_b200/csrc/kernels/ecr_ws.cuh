@@ -38,6 +38,9 @@ namespace sconv_cu {
 #define SCONV_EMPTY_ALL_LANES 0
 #endif
 
+#ifndef SCONV_WS_OPAQUE_LANE
+#define SCONV_WS_OPAQUE_LANE 1
+#endif
 #ifndef SCONV_SPARSE_PCT_WIDE  // see WsCfg::SPARSE_PCT
 #define SCONV_SPARSE_PCT_WIDE 100
 #endif
@@ -350,6 +353,15 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
   const bool t0 = (lane % PITCH) < WPW && (lane / PITCH) < WPH;
   const bool t1 = ((lane + 32) % PITCH) < WPW && ((lane + 32) / PITCH) < WPH;
   constexpr bool TWO = WPH * PITCH > 32;
+#if SCONV_WS_OPAQUE_LANE
+  // The lane index as a shuffle result: ptxas cannot rematerialise it, so the
+  // per-channel weight loads keep it in a register instead of re-reading
+  // SR_TID.X (an S2R, ~8% of the stall samples at s = 0.95) every channel.
+  // (R >= 4 only: the R = 2 configs measured +0.3..1.4% with it.)
+  const int wlane = R >= 4 ? __shfl_sync(kFull, lane, lane) : lane;
+#else
+  const int wlane = lane;
+#endif
   for (int item = blockIdx.x, it = 0; item < items; item += gridDim.x, ++it) {
   const int cta = item / kblocks, k0 = (item - cta * kblocks) * KT, kbase = it * nchunks;
   const int t = cta * WPC + warp;
@@ -380,9 +392,14 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
 
         float wr[KK][R];
 #pragma unroll
-        for (int ij = 0; ij < KK; ++ij) ws_lds_w<R>(wr[ij], wsrc + ij * KT, lane);
+        for (int ij = 0; ij < KK; ++ij) ws_lds_w<R>(wr[ij], wsrc + ij * KT, wlane);
 
-        if ((__popc(m0) + __popc(m1)) * 100 <= Cfg::NPOS * Cfg::SPARSE_PCT)
+        // SPARSE_PCT 100 / 0: one body for every channel, no density test
+        if constexpr (Cfg::SPARSE_PCT >= 100)
+          ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, true>(acc, wr, ic, m0, m1);
+        else if constexpr (Cfg::SPARSE_PCT <= 0)
+          ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, false>(acc, wr, ic, m0, m1);
+        else if ((__popc(m0) + __popc(m1)) * 100 <= Cfg::NPOS * Cfg::SPARSE_PCT)
           ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, true>(acc, wr, ic, m0, m1);
         else
           ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, false>(acc, wr, ic, m0,
