@@ -35,7 +35,23 @@
 #define SCONV_BODY_GUARD 0
 #endif
 
+#ifndef SCONV_GUARD_MIN_FFMA2
+#define SCONV_GUARD_MIN_FFMA2 8
+#endif
+
 namespace sconv_cu {
+
+// Number of (i, j) taps through which window cell (Y, X) reaches the tile.
+template <int KH, int KW, int S, int TH, int TW>
+__host__ __device__ constexpr int cell_taps(int Y, int X) {
+  int n = 0;
+  for (int i = 0; i < KH; ++i)
+    for (int j = 0; j < KW; ++j) {
+      const int dy = Y - i, dx = X - j;
+      if (dy >= 0 && dy % S == 0 && dy / S < TH && dx >= 0 && dx % S == 0 && dx / S < TW) ++n;
+    }
+  return n;
+}
 
 template <int KH, int KW, int S, int TH, int TW, int R, int WPH, int WPW, int BPITCH, int SPITCH,
           bool FAST, bool ROWSKIP, bool NOSKIP = false>
@@ -72,7 +88,11 @@ __device__ __forceinline__ void ecr_channel(float (&acc)[TH][TW][R], const float
         // branch: ptxas would otherwise if-convert the 1-3-tap border cells,
         // whose predicated FFMA2 cost their pipe cycles even when the cell is
         // zero -- most of a channel's time once density falls below ~0.2.
-        if constexpr (ROWSKIP && !NOSKIP) __syncwarp();
+        // (Only small blocks need it: SCONV_GUARD_MIN_FFMA2 = the block size,
+        // in FFMA2, from which ptxas keeps a block branched by itself.)
+        if constexpr (ROWSKIP && !NOSKIP) {
+          if (cell_taps<KH, KW, S, TH, TW>(Y, X) * R / 2 < SCONV_GUARD_MIN_FFMA2) __syncwarp();
+        }
 #endif
         const float v = row[X];
 #pragma unroll
