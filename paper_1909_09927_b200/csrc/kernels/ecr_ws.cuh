@@ -53,7 +53,9 @@ struct WsCfg {
   static constexpr int KT = 32 * R;                  // output channels per CTA
   static constexpr int WPH = (TH - 1) * S + KH;      // warp input window rows
   static constexpr int WPW = (TW - 1) * S + KW;      // warp input window cols
-  static constexpr int PITCH = WPW <= 8 ? 8 : 16;    // sub-patch row pitch (floats)
+  // sub-patch row pitch (floats): 8 or 16; 4 for tall 4-column windows
+  // (7x2 tiles: 9 rows x 4) whose 8-float rows would overflow the 64-bit mask
+  static constexpr int PITCH = WPW <= 8 ? ((WPW <= 4 && WPH * 8 > 64) ? 4 : 8) : 16;
   static constexpr int PATCH = WPH * PITCH;          // floats per (warp, channel)
   static constexpr int NPOS = WPH * WPW;
   static constexpr int IN_STAGE = (WPC * CC * PATCH + 31) / 32 * 32;  // floats, 128B aligned

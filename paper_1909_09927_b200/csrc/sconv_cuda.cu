@@ -205,9 +205,9 @@ int choose_kernel(sconv_cu_ctx* ctx, int n, int c, int k, int kh, int kw, int st
           ch.which = forced;
           ch.ws = 0;
         }
-      } else if (forced >= 'A' && forced <= 'T') {
+      } else if (forced >= 'A' && forced <= 'V') {
         const int id = forced - 'A' + 1;
-        const bool general = id >= 18;
+        const bool general = id >= 18 && id <= 20;
         if (general ? !(pecr && Pk != 2 && pick_ws_pool(k, kh, kw, stride, pw, ph) == id)
                     : !ws_applies(id, k, kh, kw, stride, Pk))
           return fail(ctx, SCONV_ERR_ARG, "forced kernel %c does not apply to this shape", forced);
