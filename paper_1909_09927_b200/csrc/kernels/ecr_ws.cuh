@@ -96,6 +96,13 @@ struct WsCfg {
   // (the 4x4 R = 4 1x1 config loses 4% that way and keeps the threshold).
   static constexpr int SPARSE_PCT =
       (TH == 2 && TW == 2) ? 0 : (R <= 2 || TH <= 2) ? (KH == 1 && KW == 1 ? 0 : 100) : SCONV_SPARSE_PCT_WIDE;
+  // Channel-loop unroll: small bodies (2x2 tiles) are latency-bound per
+  // channel (cell load -> ballot -> branch -> FFMA2), so two channels in
+  // flight let the next channel's loads issue under this one's FFMA2.
+#ifndef SCONV_WS_SMALL_UNROLL
+#define SCONV_WS_SMALL_UNROLL 2
+#endif
+  static constexpr int CU = (TH * TW <= 4) ? SCONV_WS_SMALL_UNROLL : 1;
   static constexpr int PAIRS = WPC * NPOS / 2;
   static constexpr int PAIRS_PER_LANE = (PAIRS + 31) / 32;
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
@@ -387,7 +394,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
       const float* ic = smem + s * Cfg::STAGE + warp * CC * PATCH;
       const float* wsrc = smem + s * Cfg::STAGE + Cfg::IN_STAGE;
       const int cn = min(CC, C - k * CC);
-#pragma unroll 1
+#pragma unroll Cfg::CU
       for (int c = 0; c < cn; ++c, ic += PATCH, wsrc += KK * KT) {
         const unsigned m0 = __ballot_sync(kFull, t0 && ic[lane] != 0.0f);
         const unsigned m1 = TWO ? __ballot_sync(kFull, t1 && ic[lane + 32] != 0.0f) : 0u;
@@ -396,12 +403,14 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
 #pragma unroll
         for (int ij = 0; ij < KK; ++ij) ws_lds_w<R>(wr[ij], wsrc + ij * KT, wlane);
 
-        // SPARSE_PCT 100 / 0: one body for every channel, no density test
+        // SPARSE_PCT 100: one body for every channel, no density test; 0: the
+        // predicated body, empty windows skipped
         if constexpr (Cfg::SPARSE_PCT >= 100)
           ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, true>(acc, wr, ic, m0, m1);
-        else if constexpr (Cfg::SPARSE_PCT <= 0)
-          ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, false>(acc, wr, ic, m0, m1);
-        else if ((__popc(m0) + __popc(m1)) * 100 <= Cfg::NPOS * Cfg::SPARSE_PCT)
+        else if constexpr (Cfg::SPARSE_PCT <= 0) {
+          if (m0 | m1)
+            ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, false>(acc, wr, ic, m0, m1);
+        } else if ((__popc(m0) + __popc(m1)) * 100 <= Cfg::NPOS * Cfg::SPARSE_PCT)
           ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, true>(acc, wr, ic, m0, m1);
         else
           ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, false>(acc, wr, ic, m0,
