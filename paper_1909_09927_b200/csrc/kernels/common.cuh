@@ -107,6 +107,17 @@ __device__ __forceinline__ void cp_async8(float* smem, const float* gmem, int sr
                : "memory");
 }
 
+// The same with the shared-memory destination as a byte address (the
+// producers keep stage-relative offsets and add immediates).
+__device__ __forceinline__ void cp_async4_s(unsigned smem, const float* gmem, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem), "l"(gmem), "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8_s(unsigned smem, const float* gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(float* smem, const float* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   const int bytes = valid ? 16 : 0;

@@ -45,10 +45,12 @@ namespace sconv_cu {
 #define SCONV_SPARSE_PCT_WIDE 100
 #endif
 
-template <int KH_, int KW_, int S_, int TH_, int TW_, int R_, int WPC_, int CC_, int NS_, int P_>
+template <int KH_, int KW_, int S_, int TH_, int TW_, int R_, int WPC_, int CC_, int NS_, int P_,
+          int NP_ = 1>
 struct WsCfg {
   static constexpr int KH = KH_, KW = KW_, S = S_, TH = TH_, TW = TW_, R = R_;
   static constexpr int WPC = WPC_, CC = CC_, NS = NS_, P = P_;
+  static constexpr int NP = NP_;                     // producer warps (cells split between them)
   static constexpr int KK = KH * KW;
   static constexpr int KT = 32 * R;                  // output channels per CTA
   static constexpr int WPH = (TH - 1) * S + KH;      // warp input window rows
@@ -61,7 +63,7 @@ struct WsCfg {
   static constexpr int IN_STAGE = (WPC * CC * PATCH + 31) / 32 * 32;  // floats, 128B aligned
   static constexpr int W_STAGE = CC * KK * KT;       // floats
   static constexpr int STAGE = IN_STAGE + W_STAGE;
-  static constexpr int NT = 32 * (WPC + 1);          // + producer warp
+  static constexpr int NT = 32 * (WPC + NP);         // + producer warps
   static constexpr int MINB =  // CTAs/SM (register budget: accumulators + weight registers)
       (NT > 256 || R >= 8) ? 1 : ((TH * TW * R <= 32 && KH * KW * R <= 36) ? 3 : 2);
   // P == -1 (any pool geometry): the epilogue stages each warp's conv tile in
@@ -70,7 +72,7 @@ struct WsCfg {
   static constexpr int RING = NS * STAGE > EPI ? NS * STAGE : EPI;  // floats before the barriers
   static constexpr int SMEM_BYTES = RING * 4 + 2 * NS * 8;
   static constexpr int CELLS = WPC * NPOS;           // input cells per channel
-  static constexpr int CELLS_PER_LANE = (CELLS + 31) / 32;
+  static constexpr int CELLS_PER_LANE = (CELLS + 32 * NP - 1) / (32 * NP);
   // Producer copies cells in 8-byte pairs when every window row starts on an
   // even column (even row width, even tile stride and map width): half the
   // cp.async instructions and requests.
@@ -102,9 +104,12 @@ struct WsCfg {
 #ifndef SCONV_WS_SMALL_UNROLL
 #define SCONV_WS_SMALL_UNROLL 2
 #endif
-  static constexpr int CU = (TH * TW <= 4) ? SCONV_WS_SMALL_UNROLL : 1;
+#ifndef SCONV_WS_BIG_UNROLL
+#define SCONV_WS_BIG_UNROLL 1
+#endif
+  static constexpr int CU = (TH * TW <= 4) ? SCONV_WS_SMALL_UNROLL : SCONV_WS_BIG_UNROLL;
   static constexpr int PAIRS = WPC * NPOS / 2;
-  static constexpr int PAIRS_PER_LANE = (PAIRS + 31) / 32;
+  static constexpr int PAIRS_PER_LANE = (PAIRS + 32 * NP - 1) / (32 * NP);
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
   static_assert(R == 2 || R == 4 || R == 8, "R");
   static_assert(P <= 0 || (TH % P == 0 && TW % P == 0), "pool tile");
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
   constexpr int KH = Cfg::KH, KW = Cfg::KW, S = Cfg::S, TH = Cfg::TH, TW = Cfg::TW, R = Cfg::R;
   constexpr int KK = Cfg::KK, KT = Cfg::KT, CC = Cfg::CC, NS = Cfg::NS, P = Cfg::P;
   constexpr int WPC = Cfg::WPC, WPH = Cfg::WPH, WPW = Cfg::WPW, PITCH = Cfg::PITCH;
-  constexpr int PATCH = Cfg::PATCH;
+  constexpr int PATCH = Cfg::PATCH, NP = Cfg::NP;
 
   extern __shared__ float4 smem_raw[];
   float* smem = reinterpret_cast<float*>(smem_raw);
@@ -247,14 +252,17 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 33);  // 32 cp.async lane arrivals + the TMA expect_tx arrival
+      mbar_init(&full[s], 32 * NP + 1);  // cp.async lane arrivals + the TMA expect_tx arrival
       mbar_init(&empty[s], SCONV_EMPTY_ALL_LANES ? WPC * 32 : WPC);
     }
   }
   __syncthreads();
 
-  if (warp == WPC) {
+  if (warp >= WPC) {
     // ------------------------------ producer ------------------------------
+    // producer warp pw copies cells (pairs) pw*32 + lane + 32*NP*e; pw 0 also
+    // issues the weight TMA
+    const int pl = NP == 1 ? lane : (warp - WPC) * 32 + lane;  // lane among the producer warps
     const size_t plane = static_cast<size_t>(H) * W;
     if constexpr (Cfg::PAIR) {
       // warp-uniform: 8-byte aligned cell pairs (every window row starts on
@@ -264,12 +272,15 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
           asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
         for (int item = blockIdx.x, it = 0; item < items; item += gridDim.x, ++it) {
         const int cta = item / kblocks, k0 = (item - cta * kblocks) * KT, kbase = it * nchunks;
-        int src_off[Cfg::PAIRS_PER_LANE];
-        int dst_off[Cfg::PAIRS_PER_LANE];
+        // per pair: source pointer at channel 0 (the map base for pairs outside
+        // the map: zero-filled, and base + c0 * plane stays inside the map),
+        // valid bytes, and shared-memory byte offset within a stage
+        const float* src0[Cfg::PAIRS_PER_LANE];
         int bytes[Cfg::PAIRS_PER_LANE];
+        unsigned dst_b[Cfg::PAIRS_PER_LANE];
 #pragma unroll
         for (int e = 0; e < Cfg::PAIRS_PER_LANE; ++e) {
-          const int q = lane + 32 * e;
+          const int q = pl + 32 * NP * e;
           const int wi = q / (Cfg::NPOS / 2), pp = q - wi * (Cfg::NPOS / 2);
           const int Y = pp / (WPW / 2), X = 2 * (pp - Y * (WPW / 2));
           const int t = cta * WPC + wi;
@@ -278,27 +289,29 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
           const int iy = ty * a.tsy * S + Y, ix = tx * a.tsx * S + X;
           const bool ok = q < Cfg::PAIRS && t < a.total_tiles && iy < H && ix < W;
           bytes[e] = ok ? (ix + 1 < W ? 8 : 4) : 0;
-          src_off[e] = ok ? static_cast<int>((static_cast<size_t>(n) * C * H + iy) * W + ix) : 0;
-          dst_off[e] = (wi * CC) * PATCH + Y * PITCH + X;
+          src0[e] = ok ? a.x + (static_cast<size_t>(n) * C * H + iy) * W + ix : a.x;
+          dst_b[e] = 4u * ((wi * CC) * PATCH + Y * PITCH + X);
         }
         for (int k = 0; k < nchunks; ++k) {
           const int kk = kbase + k, s = kk % NS;
           if (kk >= NS) mbar_wait_sleep(&empty[s], ((kk / NS) + 1) & 1);
           float* in_s = smem + s * Cfg::STAGE;
           float* w_s = in_s + Cfg::IN_STAGE;
+          const unsigned in_b = smem_u32(in_s);
           const int c0 = k * CC;
+          const size_t coff = static_cast<size_t>(c0) * plane;
+          const bool whole = c0 + CC <= C;  // uniform: no channel tail in this chunk
 #pragma unroll
           for (int e = 0; e < Cfg::PAIRS_PER_LANE; ++e) {
-            if (lane + 32 * e < Cfg::PAIRS) {
+            if (pl + 32 * NP * e < Cfg::PAIRS) {
+              const float* src = src0[e] + coff;
+              const unsigned dst = in_b + dst_b[e];
 #pragma unroll
-              for (int ch = 0; ch < CC; ++ch) {
-                const int b = c0 + ch < C ? bytes[e] : 0;
-                const float* src = b ? a.x + src_off[e] + (c0 + ch) * plane : a.x;
-                cp_async8(in_s + dst_off[e] + ch * PATCH, src, b);
-              }
+              for (int ch = 0; ch < CC; ++ch, src += plane)
+                cp_async8_s(dst + 4u * ch * PATCH, src, whole || c0 + ch < C ? bytes[e] : 0);
             }
           }
-          if (lane == 0) {
+          if (pl == 0) {
             mbar_arrive_expect_tx(&full[s], Cfg::W_BYTES);
             tma_load_3d(w_s, &wmap, k0, 0, c0, &full[s]);
           }
@@ -313,12 +326,12 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
     for (int item = blockIdx.x, it = 0; item < items; item += gridDim.x, ++it) {
     const int cta = item / kblocks, k0 = (item - cta * kblocks) * KT, kbase = it * nchunks;
-    int src_off[Cfg::CELLS_PER_LANE];
-    int dst_off[Cfg::CELLS_PER_LANE];
+    const float* src0[Cfg::CELLS_PER_LANE];
     bool ok[Cfg::CELLS_PER_LANE];
+    unsigned dst_b[Cfg::CELLS_PER_LANE];
 #pragma unroll
     for (int e = 0; e < Cfg::CELLS_PER_LANE; ++e) {
-      const int q = lane + 32 * e;
+      const int q = pl + 32 * NP * e;
       const int wi = q / Cfg::NPOS, pos = q - (q / Cfg::NPOS) * Cfg::NPOS;
       const int Y = pos / WPW, X = pos - (pos / WPW) * WPW;
       const int t = cta * WPC + wi;
@@ -326,27 +339,29 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
       const int ty = tt / a.tiles_x, tx = tt - ty * a.tiles_x;
       const int iy = ty * a.tsy * S + Y, ix = tx * a.tsx * S + X;
       ok[e] = q < Cfg::CELLS && t < a.total_tiles && iy < H && ix < W;
-      src_off[e] = ok[e] ? static_cast<int>((static_cast<size_t>(n) * C * H + iy) * W + ix) : 0;
-      dst_off[e] = (wi * CC) * PATCH + Y * PITCH + X;
+      src0[e] = ok[e] ? a.x + (static_cast<size_t>(n) * C * H + iy) * W + ix : a.x;
+      dst_b[e] = 4u * ((wi * CC) * PATCH + Y * PITCH + X);
     }
     for (int k = 0; k < nchunks; ++k) {
       const int kk = kbase + k, s = kk % NS;
       if (kk >= NS) mbar_wait_sleep(&empty[s], ((kk / NS) + 1) & 1);
       float* in_s = smem + s * Cfg::STAGE;
       float* w_s = in_s + Cfg::IN_STAGE;
+      const unsigned in_b = smem_u32(in_s);
       const int c0 = k * CC;
+      const size_t coff = static_cast<size_t>(c0) * plane;
+      const bool whole = c0 + CC <= C;
 #pragma unroll
       for (int e = 0; e < Cfg::CELLS_PER_LANE; ++e) {
-        if (lane + 32 * e < Cfg::CELLS) {
+        if (pl + 32 * NP * e < Cfg::CELLS) {
+          const float* src = src0[e] + coff;
+          const unsigned dst = in_b + dst_b[e];
 #pragma unroll
-          for (int ch = 0; ch < CC; ++ch) {
-            const bool v = ok[e] && c0 + ch < C;
-            const float* src = v ? a.x + src_off[e] + (c0 + ch) * plane : a.x;
-            cp_async4(in_s + dst_off[e] + ch * PATCH, src, v);
-          }
+          for (int ch = 0; ch < CC; ++ch, src += plane)
+            cp_async4_s(dst + 4u * ch * PATCH, src, ok[e] && (whole || c0 + ch < C));
         }
       }
-      if (lane == 0) {  // weights: one TMA box, zero-filled past C and Kp
+      if (pl == 0) {  // weights: one TMA box, zero-filled past C and Kp
         mbar_arrive_expect_tx(&full[s], Cfg::W_BYTES);
         tma_load_3d(w_s, &wmap, k0, 0, c0, &full[s]);
       }

@@ -13,6 +13,7 @@ bool ws_applies(int id, int K, int kh, int kw, int S, int P) {
   }
   if (!(P == 0 || P == 2)) return false;
   if (id == 21 || id == 22) return kh == 3 && kw == 3 && S == 1 && P == 0;
+  if (id == 23) return kh == 3 && kw == 3 && S == 1;
   if (id == 11) return kh == 3 && kw == 3 && S == 2;
   if (id == 12) return kh == 3 && kw == 3 && S == 3;
   if (S != 1) return false;
@@ -48,7 +49,7 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4, lon
   if (!(kh == 3 && kw == 3)) return 0;
   const char* e = std::getenv("SCONV_KERNEL");
   if (e && std::strcmp(e, "v2") == 0) return 0;
-  if (e && e[0] == 'w' && e[1] >= 'A' && e[1] <= 'V' && ws_applies(e[1] - 'A' + 1, K, kh, kw, S, P))
+  if (e && e[0] == 'w' && e[1] >= 'A' && e[1] <= 'W' && ws_applies(e[1] - 'A' + 1, K, kh, kw, S, P))
     return e[1] - 'A' + 1;
   if (e && std::strcmp(e, "v3") == 0) {
     if (K <= 64) return 3;
@@ -123,6 +124,7 @@ void plan_ws(sconv_launch_plan* out, int ws, int n, int k, int OH, int OW, int p
     case 20: plan_ws_t<WsT>(out, ws, n, k, OH, OW, pw, ph, ps); return;
     case 21: plan_ws_t<WsU>(out, ws, n, k, OH, OW, 0, 0, 1); return;
     case 22: plan_ws_t<WsV>(out, ws, n, k, OH, OW, 0, 0, 1); return;
+    case 23: plan_ws_t<WsW<0>>(out, ws, n, k, OH, OW, 0, 0, 1); return;
     case 1: plan_ws_t<WsA<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
     case 2: plan_ws_t<WsB<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;
     case 4: plan_ws_t<WsD<0>>(out, ws, n, k, OH, OW, 0, 0, 1); break;

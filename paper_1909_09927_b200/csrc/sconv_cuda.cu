@@ -205,7 +205,7 @@ int choose_kernel(sconv_cu_ctx* ctx, int n, int c, int k, int kh, int kw, int st
           ch.which = forced;
           ch.ws = 0;
         }
-      } else if (forced >= 'A' && forced <= 'V') {
+      } else if (forced >= 'A' && forced <= 'W') {
         const int id = forced - 'A' + 1;
         const bool general = id >= 18 && id <= 20;
         if (general ? !(pecr && Pk != 2 && pick_ws_pool(k, kh, kw, stride, pw, ph) == id)

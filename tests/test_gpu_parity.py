@@ -217,7 +217,7 @@ KSHAPES = [
     (1, 5, 12, 12, 256, 1.0),      # all zero
     (1, 7, 9, 9, 128, 0.0),        # dense
 ]
-KERNELS = [1, 2, 3, 4, 5, 6, "A", "B", "C", "D", "E", "F", "G", "P", "U", "V"]
+KERNELS = [1, 2, 3, 4, 5, 6, "A", "B", "C", "D", "E", "F", "G", "P", "U", "V", "W"]
 
 
 @pytest.mark.parametrize("kid", KERNELS, ids=[str(k) for k in KERNELS])

@@ -43,7 +43,10 @@ def main():
     torch.backends.cudnn.benchmark = True
     dev = torch.device("cuda:0")
     orc = c_oracle()
+    only = [o for o in os.environ.get("ONLY", "").split(",") if o]
     for name, C, K, k, size, s in LAYERS:
+        if only and name not in only:
+            continue
         x = np.stack([orc.generate(size, size, C, s, 7_000_000 + n) for n in range(N)])
         w = np.stack([orc.generate(k, k, C, 0.0, 8_000_000 + j) for j in range(K)]) - np.float32(0.5)
         ref, _ = orc.ecr_conv(x[:1], w, 1)
