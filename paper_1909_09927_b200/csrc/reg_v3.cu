@@ -62,6 +62,11 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4, lon
   // for K = 64 ECR the 4x4-tile WsD (float4 stores, 3 CTAs/SM: conv1_2 3588
   // -> 3320 us); small C goes to the small-C kernel before this is asked.
   if (K >= 128 && tiles2 * kb128 <= wave) return 16;
+  // K = 64 PECR on a big grid (tiles4 >= ~15 6x6 tiles per SM): the 6x6 tiles
+  // in one persistent CTA of 15 consumers per SM (WsW) -- conv1_2 2901 -> 2783
+  // us at s = 0.7, -5% / -6% at 0.9 / 0.95 (tools/gpu_runs/gpu_r2_abgen.sh);
+  // ECR stays on WsD (+7% with WsW).
+  if (K < 128 && C >= 16 && P == 2 && tiles4 >= 148L * 15 * 36 / 16) return 23;
   if (K < 128) return C >= 16 ? (P == 2 ? 7 : 4) : 0;
   // One CTA of 15 consumer warps per SM (WsA) beats two CTAs of 7 (WsE) once
   // there are enough channel chunks to amortise a CTA's pipeline fill and

@@ -117,9 +117,14 @@ def test_launch_plan(sc):
     # ... and the per-tile one for PECR
     p = sc.launch_plan(64, 3, 226, 226, 64, 3, 3, 1, sc.PoolConfig(2, 2, 2))
     assert p["kernel"] == 300 and p["grid_x"] == 64 * 56 * 56 // 8
-    # K = 64: v3 with 6x6 tiles (WsG)
+    # K = 64 PECR: v3 with 6x6 tiles, one persistent CTA of 15 consumers + 1
+    # producer per SM on a big grid (WsW) ...
     p = sc.launch_plan(64, 64, 226, 226, 64, 3, 3, 1, sc.PoolConfig(2, 2, 2))
-    assert p["kernel"] == 107 and p["smem_bytes"] <= 227 * 1024
+    assert p["kernel"] == 123 and p["block_threads"] == 512 and p["smem_bytes"] <= 227 * 1024
+    # ... two CTAs of 7 consumers per SM on a small one (WsG), and WsD for ECR
+    p = sc.launch_plan(1, 64, 226, 226, 64, 3, 3, 1, sc.PoolConfig(2, 2, 2))
+    assert p["kernel"] == 107 and p["block_threads"] == 256
+    assert sc.launch_plan(64, 64, 226, 226, 64, 3, 3, 1)["kernel"] == 104
     # K >= 128, C >= 128: v3 warp-specialised kernel, 15 consumer warps (4x4 tiles) + 1
     # producer, one CTA per SM; linear grid, K-blocks fastest: ceil(tiles / 15) x 4
     p = sc.launch_plan(64, 512, 30, 30, 512, 3, 3, 1)
