@@ -276,6 +276,27 @@ def useful_macs(torch, x, K):
     return float(win.sum().item()) * K
 
 
+def cudnn_kernels(torch, nl, call):
+    """Names of the CUDA kernels one call of each layer's cuDNN path launches
+    (torch.profiler / CUPTI): which algorithm cudnn.benchmark settled on."""
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        out = {}
+        for l in range(nl):
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                call(l)
+                torch.cuda.synchronize()
+            names = []
+            for e in prof.events():
+                dt = str(getattr(e, "device_type", ""))
+                if "CUDA" in dt and e.name not in names:
+                    names.append(e.name[:90])
+            out[VGG19[l][0]] = names
+        return out
+    except Exception as e:  # profiler unavailable: say so, the timing stands
+        return {"unavailable": str(e)[:120]}
+
+
 def time_fn(torch, stream, fn, reps=3, trials=1):
     """Mean ms of `reps` back-to-back launches after one warm call (best of `trials`)."""
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -469,6 +490,22 @@ def main():
                              "cudnn.benchmark=True, best of 3 trials per layer"}
         for l in range(nl):
             per_layer[VGG19[l][0]]["cudnn_us"] = round(per[l] * 1e3, 1)
+        # the algorithm cuDNN picked (its kernels, from one profiled
+        # call per layer) and, informational only, the TF32-on time
+        cudnn["kernels"] = cudnn_kernels(torch, nl, lambda l: cudnn_call(torch, l, dev_x[l], dev_w[l]))
+        torch.backends.cudnn.allow_tf32 = True
+        try:
+            for l in range(nl):
+                cudnn_call(torch, l, dev_x[l], dev_w[l])
+            per32 = [time_fn(torch, stream, lambda l=l: cudnn_call(torch, l, dev_x[l], dev_w[l]),
+                             reps=3, trials=1) for l in range(nl)]
+            cudnn["tf32_on_informational"] = {
+                "ms_per_step": sum(per32),
+                "layers_us": {VGG19[l][0]: round(per32[l] * 1e3, 1) for l in range(nl)},
+                "note": "TF32 tensor cores (10-bit mantissa products) do not meet the 1e-5 parity "
+                        "bar; shown for context only"}
+        finally:
+            torch.backends.cudnn.allow_tf32 = False
 
     # ---- e2e through the C ABI with pinned host buffers --------------------
     # Two forms of the same step, every H2D and D2H byte inside the timed
