@@ -107,7 +107,11 @@ struct WsCfg {
 #ifndef SCONV_WS_BIG_UNROLL
 #define SCONV_WS_BIG_UNROLL 1
 #endif
-  static constexpr int CU = (TH * TW <= 4) ? SCONV_WS_SMALL_UNROLL : SCONV_WS_BIG_UNROLL;
+  // (measured on the config-2 layers, tools/gpu_runs/gpu_r2_c2ab.sh: 2 for the
+  // 2x2 tiles and the 1x1 windows -- inception 4a 1x1 on 4x4 tiles -3.6% --;
+  // 3 costs the 3x3 2x2-tile AlexNet layers 10%; the 4x4 3x3 bodies lose 5%
+  // with 2)
+  static constexpr int CU = (TH * TW <= 4 || KH * KW == 1) ? SCONV_WS_SMALL_UNROLL : SCONV_WS_BIG_UNROLL;
   static constexpr int PAIRS = WPC * NPOS / 2;
   static constexpr int PAIRS_PER_LANE = (PAIRS + 32 * NP - 1) / (32 * NP);
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
