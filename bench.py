@@ -345,10 +345,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    # SCONV_BENCH_DIST=gloo (dev only): exercise the multi-rank path with every
+    # rank on the GPUs that exist (timings then share a device: not a result)
+    backend = os.environ.get("SCONV_BENCH_DIST", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    red_dev = dev if backend == "nccl" else torch.device("cpu")  # max-over-ranks tensors
     torch.backends.cudnn.allow_tf32 = False
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.benchmark = True
@@ -433,7 +442,7 @@ def main():
                 for l in range(nl)]
     total_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
+        t = torch.tensor([total_ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = t.item()
     ms_per_step = total_ms / args.steps
@@ -550,7 +559,7 @@ def main():
                 each.append(round((time.perf_counter() - t1) * 1e3, 2))
             ms = (time.perf_counter() - t0) * 1e3 / steps
             if world > 1:
-                t = torch.tensor([ms], device=dev)
+                t = torch.tensor([ms], device=red_dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = t.item()
             same = all(np.array_equal(ys[l][:2].view(np.uint32),
