@@ -25,6 +25,7 @@
 #include "kernels/ingest.cuh"
 #include "kernels/smallc.cuh"
 #include "kernels/smallc2.cuh"
+#include "kernels/pointwise.cuh"
 #include "kernels/scan.cuh"
 #include "host/tma.h"
 
@@ -161,8 +162,31 @@ struct KernelChoice {
   int which = 0;            // v2 tiled config id (reg_v2.cu)
   bool pool_after = false;  // PECR pool no epilogue fuses: conv, then pecr_pool_fold_kernel
   int P = 0;                // epilogue: 2 = fused 2x2/2 pool, -1 = fused general pool, 0 = none
-  bool tiled() const { return smallc || ws || which; }
+  int pw = 0;               // 1x1 ECR as the dense ordered GEMM (pointwise.cuh): pw_tile id
+  bool tiled() const { return smallc || ws || which || pw; }
 };
+
+// Tile of the pointwise GEMM for N*P columns and K filters (0: not used).
+// Its CTAs walk the C channels in order, 8 per stage, one barrier each, so a
+// CTA's time is set by C; it pays only with >= 2 CTAs per SM of 8x8-output
+// threads (>= 1 for 64 x 128).  Measured on the config-2 1x1 layers (tools/gpu_runs/gpu_r2_pw.sh):
+// inception 4a 1x1 (294 CTAs of 64x128) 94 -> 68 us; on 5a 1x1 (100 CTAs)
+// and 4a.7 (25) the v3 1x1 configs stay as fast or faster, and smaller
+// thread tiles (more warps, less work per barrier) were slower still.
+struct PwTile {
+  int bm, bn, tm, tn;
+};
+constexpr PwTile kPwTiles[] = {{128, 128, 8, 8}, {64, 128, 8, 8}};
+int pw_tile(long long cols, int k, bool forced) {
+  auto ctas = [&](int bm, int bn) { return ((cols + bn - 1) / bn) * ((k + bm - 1) / bm); };
+  if (k % 128 == 0 && ctas(128, 128) >= 2 * 148) return 1;
+  if (forced || ctas(64, 128) >= 148) return 2;
+  return 0;
+}
+void pw_dims(int id, int* bm, int* bn) {
+  *bm = kPwTiles[id - 1].bm;
+  *bn = kPwTiles[id - 1].bn;
+}
 
 int choose_kernel(sconv_cu_ctx* ctx, int n, int c, int k, int kh, int kw, int stride, int OH,
                   int OW, bool pecr, int pw, int ph, int ps, unsigned flags, KernelChoice* out) {
@@ -199,7 +223,21 @@ int choose_kernel(sconv_cu_ctx* ctx, int n, int c, int k, int kh, int kw, int st
         ch.pool_after = ch.tiled();
       }
     }
-    if (forced && forced != 'M') {
+    // 1x1 stride-1 ECR: the dense ordered GEMM (pointwise.cuh) -- a window
+    // is one cell per channel, so the zero-skipping kernels' per-channel
+    // ballot / test / branch chain costs more than the multiplies it skips
+    // (forced 'Y'; SCONV_NO_PW=1 keeps the v3 1x1 configs)
+    static const bool pw_off = std::getenv("SCONV_NO_PW") != nullptr;  // dev A/B
+    const int pwt = kh == 1 && kw == 1 && stride == 1 && Pk == 0
+                        ? pw_tile(static_cast<long long>(n) * OH * OW, k, forced == 'Y') : 0;
+    if (pwt && ((!forced && !pw_off) || forced == 'Y')) {
+      ch.pw = pwt;
+      ch.ws = ch.which = 0;
+      ch.smallc = false;
+    } else if (forced == 'Y') {
+      return fail(ctx, SCONV_ERR_ARG, "forced kernel Y does not apply to this shape");
+    }
+    if (forced && forced != 'M' && forced != 'Y') {
       if (forced >= 1 && forced <= kNumCfgs) {
         if (tileable) {
           ch.which = forced;
@@ -246,6 +284,11 @@ long ctas_for(const KernelChoice& ch, int nb, int k, int OH, int OW, size_t y_im
               int ps) {
   sconv_launch_plan pl{};
   if (ch.smallc) return (nb * smallc_tiles(ch, OH, OW, pw, ph, ps) + 7) / 8 * ((k + 63) / 64);
+  if (ch.pw) {
+    int bm, bn;
+    pw_dims(ch.pw, &bm, &bn);
+    return (long(nb) * OH * OW + bn - 1) / bn * ((k + bm - 1) / bm);
+  }
   if (ch.ws) {
     plan_ws(&pl, ch.ws, nb, k, OH, OW, pw, ph, ps);
     return long(pl.grid_x) * pl.grid_y * pl.grid_z;
@@ -467,6 +510,21 @@ int launch_chunk(sconv_cu_ctx* ctx, const KernelChoice& ch, cudaStream_t cs, con
       fast ? ecr_smallc_kernel<0, true><<<grid, 256, 0, cs>>>(a)
            : ecr_smallc_kernel<0, false><<<grid, 256, 0, cs>>>(a);
     TRY(finish_launch(ctx, "ecr_smallc_kernel"));
+  } else if (ch.pw) {
+    const long long cols = static_cast<long long>(nb) * OH * OW;
+    PwArgs a{dx, wt, dconv, nb, c, OH * OW, k, Kp, cols, model};
+    int bm, bn;
+    pw_dims(ch.pw, &bm, &bn);
+    const dim3 grid(static_cast<unsigned>((cols + bn - 1) / bn), static_cast<unsigned>((k + bm - 1) / bm));
+#define SCONV_PW_LAUNCH(BM, BN, TM, TN)                                                          \
+  (fast ? pw_gemm_kernel<BM, BN, TM, TN, true><<<grid, PwCfg<BM, BN, TM, TN>::NT, 0, cs>>>(a)   \
+        : pw_gemm_kernel<BM, BN, TM, TN, false><<<grid, PwCfg<BM, BN, TM, TN>::NT, 0, cs>>>(a))
+    if (ch.pw == 1)
+      SCONV_PW_LAUNCH(128, 128, 8, 8);
+    else
+      SCONV_PW_LAUNCH(64, 128, 8, 8);
+#undef SCONV_PW_LAUNCH
+    TRY(finish_launch(ctx, "pw_gemm_kernel"));
   } else if (ch.ws) {
     WsArgs a{dx, wt, dconv, nb, c, h, w, k, Kp, OH, OW, 0, 0, 0, model};
     if (ch.P < 0) a.pw = pw, a.ph = ph, a.ps = ps, a.PHo = PHo, a.PWo = PWo;
@@ -992,6 +1050,18 @@ int sconv_cu_plan(int n, int c, int h, int w, int k, int kh, int kw, int stride,
     out->smem_bytes = 8 * 48 * 4;
     out->tile_h = out->tile_w = 4;
     out->tile_k = 64;
+  } else if (ch.pw) {
+    int bm, bn;
+    pw_dims(ch.pw, &bm, &bn);
+    out->kernel = 400 + ch.pw;
+    out->grid_x = static_cast<int>((long(n) * OH * OW + bn - 1) / bn);
+    out->grid_y = (k + bm - 1) / bm;
+    out->grid_z = 1;
+    out->block_threads = bm / kPwTiles[ch.pw - 1].tm * (bn / kPwTiles[ch.pw - 1].tn);
+    out->smem_bytes = 4 * 8 * (bm + bn) * 4;
+    out->tile_h = 1;
+    out->tile_w = bn;
+    out->tile_k = bm;
   } else if (ws) {
     plan_ws(out, ws, n, k, OH, OW, ch.P < 0 ? pool_w : 0, pool_h, pool_stride);
   } else if (which) {

@@ -433,8 +433,9 @@ def test_ws_1x1_5x5(sc, orc, shape):
     x, f = inputs(orc, n, c, h, w, k, kk, kk, sp, seed=(hash(shape) ^ 91) & 0xFFFF)
     ref, rops = orc.ecr_conv(x, f, 1)
     plan = sc.launch_plan(n, c, h, w, k, kk, kk, 1)
-    # 4x4 tiles, or 2x2 tiles when those fit in one wave (small grids)
-    assert plan["kernel"] in ((110, 117) if kk == 5 else ((108, 114) if k >= 128 else (109, 115)))
+    # 5x5: 4x4 tiles, or 2x2 tiles when those fit in one wave (small grids);
+    # 1x1: the dense ordered GEMM (pointwise.cuh)
+    assert plan["kernel"] in ((110, 117) if kk == 5 else (401, 402, 108, 109, 114, 115))
     ops = sc.OpCount()
     y = sc.ecr_conv_batched(x, f, 1, counters=ops)
     assert bits_equal(y, ref)
@@ -454,6 +455,60 @@ def test_ws_1x1_5x5(sc, orc, shape):
                 assert bits_equal(sc.pecr_conv_pool_batched(x, f, 1, pool, kernel=forced), pref)
     with pytest.raises(ValueError):  # SCONV_ERR_ARG: a 3x3 config forced on a 1x1/5x5 shape
         sc.ecr_conv_batched(x, f, 1, kernel="A")
+    if kk == 1:
+        assert bits_equal(sc.ecr_conv_batched(x, f, 1, kernel="Y"), ref)
+    else:
+        with pytest.raises(ValueError):  # the pointwise GEMM is 1x1 ECR only
+            sc.ecr_conv_batched(x, f, 1, kernel="Y")
+
+
+PWSHAPES = [
+    # n, c, h, w, k, sparsity: every pointwise tile (401-403), ragged C / K / columns
+    (16, 256, 56, 56, 512, 0.7),    # 128 x 128 tiles
+    (4, 256, 28, 28, 512, 0.7),
+    (3, 13, 9, 11, 200, 0.5),       # C not a multiple of 8, K not of 4, ragged columns
+    (2, 480, 14, 14, 192, 0.9),     # GoogLeNet 4a 1x1
+    (5, 832, 7, 7, 256, 0.95),
+    (1, 1, 1, 1, 1, 0.0),           # one output
+    (2, 9, 5, 5, 33, 1.0),          # all zero
+]
+
+
+@pytest.mark.parametrize("shape", PWSHAPES, ids=[str(s) for s in PWSHAPES])
+def test_pointwise(sc, orc, shape):
+    """1x1 ECR on the dense ordered GEMM: EXACT bit-identical to the oracle
+    (zero cells multiplied, not skipped), counters exact, FAST within the bar."""
+    n, c, h, w, k, sp = shape
+    x, f = inputs(orc, n, c, h, w, k, 1, 1, sp, seed=(hash(shape) ^ 23) & 0xFFFF)
+    x[x.view(np.uint32) == 0] = -0.0 if sp < 1 else 0.0  # the reference skips -0 too
+    ref, rops = orc.ecr_conv(x, f, 1)
+    ops = sc.OpCount()
+    assert bits_equal(sc.ecr_conv_batched(x, f, 1, counters=ops, kernel="Y"), ref)
+    assert (ops.multiplications, ops.additions) == rops
+    assert close(sc.ecr_conv_batched(x, f, 1, fast=True, kernel="Y"), ref)
+    assert bits_equal(sc.ecr_conv_batched(x, f, 1), ref)  # default selection
+
+
+def test_pointwise_nonfinite_weights(sc, orc):
+    """An Inf / NaN weight times a zero cell is NaN, which the reference never
+    computes (it skips zero cells): the GEMM predicates zero cells off for a
+    stage whose weights are not all finite."""
+    n, c, h, w, k = 2, 40, 7, 7, 96
+    x, f = inputs(orc, n, c, h, w, k, 1, 1, 0.7, seed=404)
+    f[3, 17, 0, 0] = np.inf
+    f[50, 2, 0, 0] = -np.inf
+    f[95, 33, 0, 0] = np.nan
+    ref, _ = orc.ecr_conv(x, f, 1)
+    for fast in (False, True):
+        y = sc.ecr_conv_batched(x, f, 1, fast=fast, kernel="Y")
+        nan_ref, nan_y = np.isnan(ref), np.isnan(y)
+        assert (nan_ref == nan_y).all()
+        if not fast:
+            assert bits_equal(np.where(nan_ref, 0, y), np.where(nan_ref, 0, ref))
+        else:  # same Inf / NaN positions and values, the finite rest within the bar
+            fin = np.isfinite(ref)
+            assert (np.isfinite(y) == fin).all() and (y[np.isinf(ref)] == ref[np.isinf(ref)]).all()
+            assert close(np.where(fin, y, 0), np.where(fin, ref, 0))
 
 
 SSHAPES = [

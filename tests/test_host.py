@@ -151,9 +151,16 @@ def test_launch_plan(sc):
     # 5x5 / 1x1 windows: the v3 kernel instantiated for them; other shapes: generic
     assert sc.launch_plan(64, 32, 18, 18, 128, 5, 5, 1)["kernel"] == 110
     assert sc.launch_plan(64, 48, 7, 7, 128, 5, 5, 1)["kernel"] == 117
-    assert sc.launch_plan(64, 480, 14, 14, 192, 1, 1, 1)["kernel"] == 108
+    # 1x1 ECR: the dense ordered GEMM when its grid holds >= 2 CTAs per SM
+    # (401 = 128x128, 402 = 64x128 filters x columns); below that the v3 1x1
+    # configs; 1x1 PECR: v3
+    p = sc.launch_plan(64, 480, 14, 14, 192, 1, 1, 1)
+    assert p["kernel"] == 402 and p["grid_x"] == 64 * 196 // 128 and p["grid_y"] == 3
+    assert p["block_threads"] == 128
     assert sc.launch_plan(64, 832, 7, 7, 256, 1, 1, 1)["kernel"] == 114
     assert sc.launch_plan(64, 480, 7, 7, 64, 1, 1, 1)["kernel"] == 115
+    assert sc.launch_plan(16, 256, 56, 56, 512, 1, 1, 1)["kernel"] == 401
+    assert sc.launch_plan(64, 480, 14, 14, 192, 1, 1, 1, sc.PoolConfig(2, 2, 2))["kernel"] in (108, 114)
     assert sc.launch_plan(1, 3, 227, 227, 96, 11, 11, 4)["kernel"] == 0
 
 
