@@ -82,7 +82,8 @@ typedef enum {
  * TiledCfg1..6 (ignored when the shape is not a 3x3 stride-1 tile);
  * 'A'..'L', 'N'..'Q' = v3 WsA..WsQ, 'R'..'T' = the general-pool WsR..WsT
  * (PECR with a pool other than 2x2/2), 'U' / 'V' = the ECR-only 2x7 / 7x2
- * tiles, 'W' = 6x6 tiles with two producer warps (csrc/reg_v3.inc;
+ * tiles, 'W' = 6x6 tiles in one 15-consumer CTA per SM, 'Y' = the 1x1
+ * dense ordered GEMM (kernels/pointwise.cuh) (csrc/reg_v3.inc;
  * SCONV_ERR_ARG when the config does not fit the
  * window / stride / pool); 'M' = the small-C kernel.
  * 0 (default) lets the launch layer pick. */
