@@ -42,7 +42,16 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float w0, float w1, 
 // FMUL2 and two scalar FADDs.  (A packed mul.rn.f32x2 followed by a packed
 // add.rn.f32x2 is NOT used: ptxas 12.9 fuses that pair into an FFMA2 even
 // with -fmad=false, which would round once instead of twice.)
-__device__ __forceinline__ void exact2(float& a0, float& a1, float w0, float w1, float v) {
+//
+// exact2_mul: that FMUL2 + two FADDs.  exact2: two issue slots -- the products
+// by a packed FFMA with a -0 addend (w*v + -0 rounds exactly like w*v, +0
+// products included), then one packed FADD; the -0 is read from constant
+// memory, whose contents ptxas cannot assume, so it cannot turn the FFMA2 into
+// an FMUL2 and fuse it with the add.  The branchy ECR bodies are issue-bound
+// and take exact2 (EXACT conv1_2 -12%, conv4_2 -7%); the dense small-C kernel
+// is FMA-pipe-bound, where FFMA2 + FADD2 cost more pipe cycles than FMUL2 +
+// two FADDs (conv1_1 +24%), and keeps exact2_mul.
+__device__ __forceinline__ void exact2_mul(float& a0, float& a1, float w0, float w1, float v) {
   asm("{\n\t.reg .b64 w, v, t;\n\t.reg .f32 t0, t1;\n\t"
       "mov.b64 w, {%2, %3};\n\t"
       "mov.b64 v, {%4, %4};\n\t"
@@ -52,6 +61,26 @@ __device__ __forceinline__ void exact2(float& a0, float& a1, float w0, float w1,
       "add.rn.f32 %1, %1, t1;\n\t}"
       : "+f"(a0), "+f"(a1)
       : "f"(w0), "f"(w1), "f"(v));
+}
+#ifndef SCONV_EXACT_FMA
+#define SCONV_EXACT_FMA 1
+#endif
+__constant__ float c_sconv_negzero = -0.0f;
+__device__ __forceinline__ void exact2(float& a0, float& a1, float w0, float w1, float v) {
+#if SCONV_EXACT_FMA
+  asm("{\n\t.reg .b64 w, v, z, t, a;\n\t"
+      "mov.b64 w, {%2, %3};\n\t"
+      "mov.b64 v, {%4, %4};\n\t"
+      "mov.b64 z, {%5, %5};\n\t"
+      "fma.rn.f32x2 t, w, v, z;\n\t"
+      "mov.b64 a, {%0, %1};\n\t"
+      "add.rn.f32x2 a, a, t;\n\t"
+      "mov.b64 {%0, %1}, a;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(w0), "f"(w1), "f"(v), "f"(c_sconv_negzero));
+#else
+  exact2_mul(a0, a1, w0, w1, v);
+#endif
 }
 
 // Keeps ptxas from if-converting a zero-skip block into predicated FMAs

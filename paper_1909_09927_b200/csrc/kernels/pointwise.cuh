@@ -15,7 +15,7 @@
 //   and a round-to-nearest sum is -0 only when both addends are), so the
 //   result is bit-identical.  A stage whose weights hold an Inf / NaN (whose
 //   product with 0 is NaN) runs with the zero cells predicated off instead;
-// * EXACT: rounded product then rounded sum (FMUL2 + two FADD, exact2);
+// * EXACT: rounded product then rounded sum (exact2: FFMA2 with a -0 addend + FADD2);
 //   FAST: FFMA2.
 //
 // Tiling: CTA BM output channels x BN output columns (columns = the N*P

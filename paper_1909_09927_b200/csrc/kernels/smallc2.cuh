@@ -100,7 +100,7 @@ __device__ __forceinline__ void mac2(float& a0, float& a1, float w0, float w1, f
   if constexpr (FAST) {
     ffma2(a0, a1, w0, w1, v);
   } else {
-    exact2(a0, a1, w0, w1, v);
+    exact2_mul(a0, a1, w0, w1, v);  // FMA-pipe-bound here: see common.cuh
   }
 }
 

@@ -26,6 +26,7 @@ def child():
     s = float(os.environ.get("S", "0.7"))
     n = int(os.environ.get("N", "64"))
     pecr_env = os.environ.get("PECR", "auto")
+    fast = os.environ.get("EXACT", "0") != "1"  # EXACT=1: time the bit-exact mode
     dev = torch.device("cuda:0")
     out = {}
     for name in names:
@@ -35,9 +36,9 @@ def child():
         w = torch.from_numpy(vgg_filters(l)).to(dev)
         pecr = pooled if pecr_env == "auto" else pecr_env == "1"
         if pecr:
-            fn = lambda: sc.pecr_conv_pool_batched(x, w, 1, sc.PoolConfig(2, 2, 2), fast=True, sync=False)
+            fn = lambda: sc.pecr_conv_pool_batched(x, w, 1, sc.PoolConfig(2, 2, 2), fast=fast, sync=False)
         else:
-            fn = lambda: sc.ecr_conv_batched(x, w, 1, fast=True, sync=False)
+            fn = lambda: sc.ecr_conv_batched(x, w, 1, fast=fast, sync=False)
         for _ in range(2):
             y = fn()
         ts = []
