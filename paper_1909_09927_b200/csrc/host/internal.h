@@ -73,6 +73,12 @@ struct sconv_cu_ctx {
   cudaGraphExec_t fwd_graph = nullptr;  // SCONV_F_GRAPH: the captured forward
   std::string fwd_key;                  // ... and the arguments it was captured for
   cudaEvent_t ev_graph = nullptr;
+  // Row-prefetch gates of ecr_ws_kernel launches (ws_density_gate_kernel
+  // writes one, the two variants read it), taken round robin: a slot is
+  // reused only kGates launches later on the context's stream.
+  static constexpr int kGates = 64;
+  int* gate = nullptr;
+  unsigned gate_next = 0;
 };
 
 namespace sconv_cu {

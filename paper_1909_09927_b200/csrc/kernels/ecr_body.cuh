@@ -48,6 +48,24 @@
 
 namespace sconv_cu {
 
+// One window row (WPW cells, 16B-aligned) from shared memory by volatile
+// loads, so ptxas keeps them where they are issued (row prefetch below).
+template <int WPW>
+__device__ __forceinline__ void lds_row_pinned(float (&dst)[4 * ((WPW + 3) / 4)], const float* src) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(src));
+#pragma unroll
+  for (int q = 0; q < (WPW + 3) / 4; ++q) {
+    if (4 * q + 2 >= WPW) {
+      asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(dst[4 * q]), "=f"(dst[4 * q + 1]) : "r"(a + 16 * q));
+      dst[4 * q + 2] = dst[4 * q + 3] = 0.0f;
+    } else {
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(dst[4 * q]), "=f"(dst[4 * q + 1]), "=f"(dst[4 * q + 2]), "=f"(dst[4 * q + 3])
+                   : "r"(a + 16 * q));
+    }
+  }
+}
+
 // Number of (i, j) taps through which window cell (Y, X) reaches the tile.
 template <int KH, int KW, int S, int TH, int TW>
 __host__ __device__ constexpr int cell_taps(int Y, int X) {
@@ -61,25 +79,36 @@ __host__ __device__ constexpr int cell_taps(int Y, int X) {
 }
 
 template <int KH, int KW, int S, int TH, int TW, int R, int WPH, int WPW, int BPITCH, int SPITCH,
-          bool FAST, bool ROWSKIP, bool NOSKIP = false>
+          bool FAST, bool ROWSKIP, bool NOSKIP = false, bool RP = false>
 __device__ __forceinline__ void ecr_channel(float (&acc)[TH][TW][R], const float (&wr)[KH * KW][R],
                                             const float* is, unsigned m0, unsigned m1) {
   static_assert(WPH * BPITCH <= 64, "window mask must fit 64 bits");
   constexpr int W4 = (WPW + 3) / 4;
   const unsigned long long mm = (static_cast<unsigned long long>(m1) << 32) | m0;
+  // RP: row Y+1 is read while row Y runs (its load latency leaves the row
+  // start), at the price of one wasted read per empty row
+  float nrow[4 * W4];
+  if constexpr (RP) lds_row_pinned<WPW>(nrow, is);
 #pragma unroll
   for (int Y = 0; Y < WPH; ++Y) {
+    float row[4 * W4];
+    if constexpr (RP) {
+#pragma unroll
+      for (int q = 0; q < 4 * W4; ++q) row[q] = nrow[q];
+      if (Y + 1 < WPH) lds_row_pinned<WPW>(nrow, is + (Y + 1) * SPITCH);
+    }
     if constexpr (ROWSKIP) {
       if (((mm >> (Y * BPITCH)) & ((1ull << WPW) - 1ull)) == 0ull) continue;  // empty row
     }
-    float row[4 * W4];
+    if constexpr (!RP) {
 #pragma unroll
-    for (int q = 0; q < W4; ++q) {
-      const float4 v4 = *reinterpret_cast<const float4*>(is + Y * SPITCH + 4 * q);
-      row[4 * q + 0] = v4.x;
-      row[4 * q + 1] = v4.y;
-      row[4 * q + 2] = v4.z;
-      row[4 * q + 3] = v4.w;
+      for (int q = 0; q < W4; ++q) {
+        const float4 v4 = *reinterpret_cast<const float4*>(is + Y * SPITCH + 4 * q);
+        row[4 * q + 0] = v4.x;
+        row[4 * q + 1] = v4.y;
+        row[4 * q + 2] = v4.z;
+        row[4 * q + 3] = v4.w;
+      }
     }
 #pragma unroll
     for (int X = 0; X < WPW; ++X) {

@@ -41,6 +41,14 @@ namespace sconv_cu {
 #ifndef SCONV_WS_OPAQUE_LANE
 #define SCONV_WS_OPAQUE_LANE 1
 #endif
+// Window-row prefetch: 0 never, 1 always, 2 per launch from the sampled
+// input density (at least SCONV_WS_RP_DENSITY_PCT percent nonzero)
+#ifndef SCONV_WS_RP
+#define SCONV_WS_RP 2
+#endif
+#ifndef SCONV_WS_RP_DENSITY_PCT
+#define SCONV_WS_RP_DENSITY_PCT 15
+#endif
 #ifndef SCONV_SPARSE_PCT_WIDE  // see WsCfg::SPARSE_PCT
 #define SCONV_SPARSE_PCT_WIDE 100
 #endif
@@ -112,6 +120,9 @@ struct WsCfg {
   // 3 costs the 3x3 2x2-tile AlexNet layers 10%; the 4x4 3x3 bodies lose 5%
   // with 2)
   static constexpr int CU = (TH * TW <= 4 || KH * KW == 1) ? SCONV_WS_SMALL_UNROLL : SCONV_WS_BIG_UNROLL;
+  // the window-row prefetch (ecr_channel RP) is measured, and instantiated,
+  // for the 3x3 stride-1 one-body configs
+  static constexpr bool RPOK = SPARSE_PCT >= 100 && KH == 3 && KW == 3 && S == 1 && P >= 0;
   static constexpr int PAIRS = WPC * NPOS / 2;
   static constexpr int PAIRS_PER_LANE = (PAIRS + 32 * NP - 1) / (32 * NP);
   static_assert(PATCH <= 64, "sub-patch must fit the two 32-bit ballots");
@@ -134,6 +145,10 @@ struct WsArgs {
   // = TH, TW for P >= 0): overlapping pools recompute the shared conv rows
   // instead of sending the pre-pool map through HBM.
   int pw = 0, ph = 0, ps = 1, PHo = 0, PWo = 0, tsy = 0, tsx = 0;
+  // Row-prefetch gate (RPOK configs): the plain and the row-prefetching
+  // instantiation are both launched and every CTA of the one not chosen by
+  // ws_density_gate_kernel (*gate = 1: prefetch) exits at once; nullptr: run.
+  const int* gate = nullptr;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -222,9 +237,29 @@ __device__ __forceinline__ void ws_lds_w(float (&dst)[R], const float* row, int 
 #define SCONV_WS_GUARD 2
 #endif
 
-template <class Cfg, bool FAST>
+// Window-row prefetch (RP, ecr_channel) pays while most window rows hold a
+// nonzero (-3..-5% at s = 0.5-0.8) and costs a wasted shared-memory read per
+// empty row, which the LSU-bound high-sparsity case cannot afford (+5% at
+// s = 0.9, +17% at 0.95).  Choosing it inside one kernel -- per channel, per
+// chunk, or per launch with both consumer loops compiled into one function --
+// cost 1-14% on every path (profiles/r02/ab_row_prefetch.txt), so the two
+// loops are separate instantiations and the launch picks one on the device
+// (WsArgs::gate) from the sampled input density.
+template <class Cfg>
+__global__ void ws_density_gate_kernel(const float* x, unsigned total, int* gate) {
+  // 1024 threads, one sample each: one per stratum of the input, at a hashed
+  // offset; gate = 1 iff at least SCONV_WS_RP_DENSITY_PCT percent are nonzero
+  const unsigned i = threadIdx.x, n = blockDim.x, stratum = total / n;
+  const unsigned q = stratum ? i * stratum + (i * 0x9E3779B1u) % stratum : i;
+  const int nz = __syncthreads_count(q < total && x[q] != 0.0f);
+  if (i == 0) *gate = 100 * nz >= SCONV_WS_RP_DENSITY_PCT * int(stratum ? n : total);
+}
+
+template <class Cfg, bool FAST, bool RP = false>
 __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
     ecr_ws_kernel(const WsArgs a, const __grid_constant__ CUtensorMap wmap) {
+  static_assert(!RP || Cfg::RPOK, "row prefetch is instantiated for the 3x3 one-body configs");
+  if (a.gate && (*a.gate != 0) != RP) return;  // the other instantiation runs this launch
   constexpr int KH = Cfg::KH, KW = Cfg::KW, S = Cfg::S, TH = Cfg::TH, TW = Cfg::TW, R = Cfg::R;
   constexpr int KK = Cfg::KK, KT = Cfg::KT, CC = Cfg::CC, NS = Cfg::NS, P = Cfg::P;
   constexpr int WPC = Cfg::WPC, WPH = Cfg::WPH, WPW = Cfg::WPW, PITCH = Cfg::PITCH;
@@ -425,7 +460,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB)
         // SPARSE_PCT 100: one body for every channel, no density test; 0: the
         // predicated body, empty windows skipped
         if constexpr (Cfg::SPARSE_PCT >= 100)
-          ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, true>(acc, wr, ic, m0, m1);
+          ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, true, false, RP>(acc, wr, ic,
+                                                                                       m0, m1);
         else if constexpr (Cfg::SPARSE_PCT <= 0) {
           if (m0 | m1)
             ecr_channel<KH, KW, S, TH, TW, R, WPH, WPW, PITCH, PITCH, FAST, false>(acc, wr, ic, m0, m1);

@@ -917,6 +917,13 @@ int sconv_cu_ctx_create(int device, sconv_cu_ctx** out) {
     return fail(nullptr, SCONV_ERR_CUDA, "%s", cudaGetErrorString(e));
   }
   ctx->stream = ctx->own;
+  e = cudaMalloc(&ctx->gate, sconv_cu_ctx::kGates * sizeof(int));
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(ctx->own);
+    cudaMemPoolDestroy(ctx->pool);
+    delete ctx;
+    return fail(nullptr, SCONV_ERR_CUDA, "%s", cudaGetErrorString(e));
+  }
   if (const char* e = std::getenv("SCONV_HOST_ARENAS"))  // dev knob (tools/async_probe.py)
     ctx->hws_n = std::max(1, std::min(sconv_cu_ctx::kHostArenas, std::atoi(e)));
   *out = ctx;
@@ -941,6 +948,7 @@ int sconv_cu_ctx_destroy(sconv_cu_ctx* ctx) {
     ctx->fcache.clear();
     if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     if (ctx->fwd) cudaFree(ctx->fwd);
+    if (ctx->gate) cudaFree(ctx->gate);
     if (ctx->fwd_graph) cudaGraphExecDestroy(ctx->fwd_graph);
     if (ctx->ev_graph) cudaEventDestroy(ctx->ev_graph);
     if (ctx->own) cudaStreamDestroy(ctx->own);

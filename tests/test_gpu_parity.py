@@ -652,7 +652,9 @@ def test_pecr_other_pools(sc, orc, shape):
     l0 = ctx.launches
     sc.pecr_conv_pool_batched(x, f, s, sc.PoolConfig(pw, ph, ps))
     # filter re-layout + the conv kernel; + pecr_pool_fold_kernel when not fused
-    assert ctx.launches - l0 == (2 if fused else 3), plan
+    # (whose 3x3 stride-1 conv is a row-prefetch-gated one: + the density
+    # gate and the variant not chosen)
+    assert ctx.launches - l0 in ((2,) if fused else (3, 5)), plan
     for mode in (0, 1):
         pref, rops = orc.pecr_conv(x, f, s, pw, ph, ps, mode)
         pool = sc.PoolConfig(pw, ph, ps, sc.PoolMode(mode))
