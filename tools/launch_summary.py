@@ -3,14 +3,14 @@ profiles/rNN/launches_latest.txt: the launches of the last bench step.
 
     python tools/launch_summary.py gpurun_out/launches.csv > profiles/r02/launches_latest.txt
 
-The list holds warmup + timed steps of our kernels only; one step of the
-VGG-19 bench is 32 launches (16 layers x filter transpose + conv kernel), so
-the last 32 rows are the timed step.
+The list holds warmup + timed steps of our kernels only; a step starts with
+conv1_1 (filter transpose + the small-C kernel) and runs 2-4 launches per
+layer (transpose, conv kernel; the 3x3 layers with a row-prefetch gate add
+ws_density_gate_kernel and the instantiation that exits at once), so the
+timed step is everything from the last conv1_1 transpose on.
 """
 import csv
 import sys
-
-PER_STEP = 32
 
 
 def main(path):
@@ -18,7 +18,10 @@ def main(path):
     ix = {k: i for i, k in enumerate(rows[0])}
     seq = [(r[ix["Kernel Name"]], float(r[ix["Metric Value"]].replace(",", "")))
            for r in rows[1:] if r[ix["Metric Name"]] == "gpu__time_duration.sum"]
-    last = seq[-PER_STEP:]
+    first = max(i for i, (n, _) in enumerate(seq) if "smallc" in n)
+    if first > 0 and "transpose" in seq[first - 1][0]:
+        first -= 1
+    last = seq[first:]
     tot = sum(t for _, t in last) / 1e3
     print("# ncu launch list, one bench step (the last of warmup 3 + 1 timed), our kernels only")
     print("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised: compare shares)")
