@@ -83,6 +83,12 @@ int pick_ws(int K, int C, int OW, int kh, int kw, int S, int P, long tiles4, lon
   // persistent grid WsA runs for C <= 128 (reg_v3.inc), its ring no longer
   // refills per CTA and it also wins at C = 64 (conv2_1 1254 vs WsE 1355 us,
   // tools/gpu_runs/gpu_r2_c12.sh).
+  // 14-wide maps (VGG conv5) in ECR: 7x2 tiles in the same 15-consumer CTA
+  // (WsV: 14 tiles per image instead of sixteen 4x4 tiles, no overhang) once
+  // the lean producer and the row prefetch were in: conv5_1 -1.2 / -3.4 /
+  // -3.6 / -2.4% at s = 0.5 / 0.7 / 0.8 / 0.9 (tools/gpu_runs/gpu_r2_v_rp.sh;
+  // it lost 3-11% at s >= 0.9 before them).
+  if (C >= 128 && P == 0 && OW % 7 == 0 && OW % 4 != 0 && tiles4 >= 148L * 10) return 22;
   return (C >= 64 && tiles4 >= 148L * 10) ? 1 : 5;
 }
 

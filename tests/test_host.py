@@ -136,8 +136,12 @@ def test_launch_plan(sc):
     # C < 64: two CTAs of 7 consumers per SM (WsE)
     p = sc.launch_plan(64, 32, 114, 114, 128, 3, 3, 1)
     assert p["kernel"] == 105 and p["block_threads"] == 256
-    p = sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1)  # 14x14 maps, big grid: 15-warp CTAs
-    assert p["kernel"] == 101
+    # 14x14 maps, big grid, ECR: 15-warp CTAs on 7x2 tiles (WsV: 14 per image, no overhang)
+    p = sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1)
+    assert p["kernel"] == 122 and p["block_threads"] == 512 and (p["tile_h"], p["tile_w"]) == (7, 2)
+    assert p["grid_x"] == (64 * 14 + 14) // 15 * 4
+    # ... and PECR (conv5_4) keeps the 4x4 tiles, whose 2x2 pools stay whole
+    assert sc.launch_plan(64, 512, 16, 16, 512, 3, 3, 1, sc.PoolConfig(2, 2, 2))["kernel"] == 101
     # under ~2/3 of a wave of 15-warp CTAs: two 7-warp CTAs per SM (WsE)
     p = sc.launch_plan(16, 512, 16, 16, 512, 3, 3, 1)
     assert p["kernel"] == 105 and p["grid_x"] == (16 * 16 + 6) // 7 * 4 and p["grid_y"] == 1
